@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""bench.py -- verified tokens/s of the StarSD speculative-sampling verify step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step is one sd_verify call (the whole hot path, rows a1-a10 of SURVEY 8(a)) over one batch of
+synthetic logits that is already resident in HBM.  The default workload is BASELINE.json
+configs[1] (Vicuna-7B shape: V=32000, k=5, B=64, T=1, fp32, kappa=30).  Eight distinct batches
+(720 MB > the 126 MB L2) are rotated so no step reads L2-resident inputs of the previous one.
+K steps are captured in one CUDA graph and timed with CUDA events on the launching stream;
+multi-GPU runs (torchrun) run one independent verifier per GPU (the verify step shards by
+request; no data-path collective) and report the max time over ranks.
+
+Printed: one JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "verified tokens/s (spec-sampling verify)"
+UNIT = "verified tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--temperature", type=float, default=None)
+    ap.add_argument("--nbatch", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def workload(args):
+    from workload import CONFIGS
+    c = dict(CONFIGS[args.config])
+    if args.temperature is not None:
+        c["T"] = args.temperature
+    return c
+
+
+def esize(dtype):
+    return 4 if dtype == "f32" else 2
+
+
+def algorithmic_bytes(L, V, k, e, greedy):
+    """bytes the method itself must move for one request with accept length L
+    (lazy: rows up to the first rejection), plus ids and outputs."""
+    import numpy as np
+    L = np.asarray(L, np.int64)
+    rows = (L + 1) if greedy else (L + 1) + np.minimum(L + 1, k)
+    return rows * V * e + 4 * k + 4 * (k + 2)
+
+
+def load_peaks():
+    try:
+        m = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """NVML SM-clock and throttle-reason sampling during the timed region."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x1: "gpu_idle"}
+
+    def __init__(self, index, period=0.002):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- CPU oracle ----
+def oracle_rate(d, T, seconds, seed, cores, per_step=None, steps=None):
+    """Time the CPU oracle (as it stands) on bounded samples of the workload: each step
+    verifies `per_step` consecutive requests of the batch (rotating).  Returns tokens/s and a
+    description of the sample."""
+    import numpy as np
+    import oracle
+    B = d["ids"].shape[0]
+    per_step = per_step or min(B, cores)
+    n, tok, t0, i = 0, 0, time.perf_counter(), 0
+    while True:
+        lo = (i * per_step) % B
+        idx = [(lo + j) % B for j in range(per_step)]
+        L, _, st = oracle.verify(d["p"][idx], None if T == 0 else d["q"][idx], d["ids"][idx], T,
+                                 seed=seed, round=i, rid_base=lo, n_threads=cores)
+        tok += int((L + 1)[st & oracle.HARD_FAULTS == 0].sum())
+        n += per_step
+        i += 1
+        el = time.perf_counter() - t0
+        if (steps is not None and i >= steps) or (steps is None and el >= seconds):
+            break
+    return tok / el, dict(requests=n, steps=i, per_step=per_step, seconds=el)
+
+
+def host_batch(d):
+    import numpy as np
+    import torch
+    out = {}
+    for key in ("p", "q", "ids"):
+        t = d[key]
+        if t is None:
+            out[key] = None
+        elif isinstance(t, np.ndarray):
+            out[key] = t
+        else:
+            t = t.cpu()
+            out[key] = (t.view(torch.int16).numpy().view(np.uint16)
+                        if t.dtype == torch.bfloat16 else t.numpy())
+    return out
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (the tier's reference arm) timed as it stands on this
+    host's cores, on the same config/metric; rank 0 only."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    from workload import make_batch
+    c = workload(args)
+    d = make_batch(V=c["V"], k=c["k"], B=c["B"], T=c["T"], kappa=c["kappa"] or 30.0,
+                   seed=c["seed"], dtype=args.dtype)
+    cores = len(os.sched_getaffinity(0))
+    per = max(1, min(c["B"], cores))
+    oracle_rate(d, c["T"], 0, 1, cores, per_step=per, steps=max(1, args.warmup))
+    rate, info = oracle_rate(d, c["T"], 0, 1, cores, per_step=per, steps=args.steps)
+    sample = (f"{args.steps} steps x {per} requests of the {args.config} batch "
+              f"(V={c['V']}, k={c['k']}, T={c['T']}), oracle threads={cores}")
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * info["seconds"] / info["steps"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args, c),
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, c):
+    return {"workload": f"{args.config}: {c['name']}", "vocab": c["V"], "k": c["k"],
+            "batch_per_gpu": c["B"], "temperature": c["T"], "kappa": c["kappa"],
+            "logits": args.dtype, "inputs": "synthetic log-Dirichlet logits (DESIGN.md recipe)",
+            "l2": f"rotating {args.nbatch} distinct resident input batches (> 126 MB L2)",
+            "parallelism": f"dp{args.gpus} (one verifier per GPU, requests sharded)"}
+
+
+# --------------------------------------------------------------------------------- ours ----
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2601_21622_b200 as sd
+    from paper_2601_21622_b200 import _lib
+    from workload import make_batch_torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    c = workload(args)
+    V, k, B, T = c["V"], c["k"], c["B"], c["T"]
+    greedy = T == 0.0
+    e = esize(args.dtype)
+
+    batches = [make_batch_torch(V, k, B, T, c["kappa"] or 30.0, c["seed"] + 1000 * rank + i, dev,
+                                dtype=args.dtype) for i in range(args.nbatch)]
+    torch.cuda.synchronize()
+    K, W = args.steps, max(3, args.warmup)
+    L_all = torch.empty(K, B, dtype=torch.int32, device=dev)
+    tok_all = torch.empty(K, B, k + 1, dtype=torch.int32, device=dev)
+    st_all = torch.empty(K, B, dtype=torch.int32, device=dev)
+    ws = sd.Workspace(B, k, V, T, batches[0]["p"].dtype, dev)
+    rid0 = rank << 32
+
+    def step(i, out):
+        bt = batches[i % args.nbatch]
+        return sd.verify(bt["p"], None if greedy else bt["q"], bt["ids"], T, seed=21622,
+                         round=i, request_id_base=rid0, out=out, workspace=ws)
+
+    # warm-up (eager), then capture K steps into one graph with per-step profiling events
+    wout = (L_all[0], tok_all[0], st_all[0])
+    for i in range(W):
+        step(i, wout)
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range(2 * K):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        evs.append(ev)
+    torch.cuda.synchronize()
+    import ctypes
+    handles = (ctypes.c_void_p * (2 * K))(*[ev.cuda_event for ev in evs])
+    L = _lib.load()
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream(dev)
+    cs.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(cs):
+        _lib.check(L.sd_profile_events(handles, K), "sd_profile_events")
+        with torch.cuda.graph(g, stream=cs):
+            for i in range(K):
+                step(i, (L_all[i], tok_all[i], st_all[i]))
+        _lib.check(L.sd_profile_events(None, 0), "sd_profile_events")
+    torch.cuda.synchronize()
+    g.replay()                       # one untimed replay (graph upload / first-touch)
+    torch.cuda.synchronize()
+
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0.record()
+        g.replay()
+        t1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    kA = [evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(K)]
+
+    Lh = L_all.cpu().numpy()
+    sth = st_all.cpu().numpy()
+    ok = (sth & 7) == 0
+    tokens = int((Lh + 1)[ok].sum())
+    alg = float(algorithmic_bytes(Lh, V, k, e, greedy).sum())
+    stats = torch.tensor([ms, tokens, alg, sum(kA)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = stats.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM)
+        ms_max = float(mx[0])
+    else:
+        ms_max = float(stats[0])
+    tokens_all = float(stats[1])
+    value = tokens_all / (ms_max / 1000.0)
+
+    # dominant kernel (k_row_stats): algorithmic bytes of the whole step per launch / its time
+    kA_mean_ms = statistics.fmean(kA)
+    alg_per_launch = alg / K
+    peak, peak_kind = load_peaks()
+    achieved_gbs = alg_per_launch / (kA_mean_ms / 1000.0) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_{args.dtype}.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("k_row_stats_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # e2e: host (pinned) inputs -> device -> verify -> host results, every step
+    e2e = None
+    if not args.no_e2e:
+        hb = []
+        for i in range(2):
+            bt = batches[i]
+            hb.append({x: (bt[x].cpu().pin_memory() if bt[x] is not None else None)
+                       for x in ("p", "q", "ids")})
+        staging = {}
+        for i in range(2):
+            sd.verify_host(hb[i]["p"], None if greedy else hb[i]["q"], hb[i]["ids"], T,
+                           seed=21622, round=i, request_id_base=rid0, device=dev,
+                           staging=staging)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        E = args.e2e_steps
+        etok = 0
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for i in range(E):
+            h = hb[i % 2]
+            Lo, _, so = sd.verify_host(h["p"], None if greedy else h["q"], h["ids"], T,
+                                       seed=21622, round=i, request_id_base=rid0, device=dev,
+                                       staging=staging)
+            etok += int((Lo + 1)[(so & 7) == 0].sum())
+        s1.record()
+        torch.cuda.synchronize()
+        ems = s0.elapsed_time(s1)
+        es = torch.tensor([ems, etok], dtype=torch.float64, device=dev)
+        if world > 1:
+            emx = es.clone()
+            dist.all_reduce(emx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(es, op=dist.ReduceOp.SUM)
+            ems = float(emx[0])
+        h2d = sum(t.numel() * t.element_size() for t in hb[0].values() if t is not None)
+        d2h = B * 4 + B * (k + 1) * 4 + B * 4
+        e2e = {"value": float(es[1]) / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": E}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        d0 = host_batch(batches[0])
+        cores = len(os.sched_getaffinity(0))
+        rate, info = oracle_rate(d0, T, args.cpu_seconds, 21622, cores)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{info['requests']} requests of batch 0 ({info['steps']} calls x "
+                         f"{info['per_step']}), {info['seconds']:.1f} s on {cores} threads"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": config_block(args, c),
+            "roofline": {"bound": "hbm", "kernel": "k_row_stats", "achieved": achieved_gbs,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved_gbs / peak, "traffic": traffic,
+                         "alg_bytes_per_launch": alg_per_launch,
+                         "kernel_ms_mean": kA_mean_ms,
+                         "step_gbs": alg_per_launch / (ms_max / K / 1000.0) / 1e9},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": K * 2,
+            "clocks": clocks,
+            "accept": {"mean_L": float(Lh.mean()), "mean_emitted": float((Lh + 1).mean()),
+                       "fault_requests": int((~ok).sum())},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -69,6 +69,9 @@ def lib():
         L.sd_ref_sample_check.argtypes = [vp, vp, vp, i32, i32, i32, i64, i64, i32, dbl, u64, u64,
                                           u64, i32, i32, vp, vp, vp, vp]
         L.sd_ref_sample_check.restype = ctypes.c_int
+        L.sd_ref_accept_probs.argtypes = [vp, vp, vp, i32, i32, i32, i64, i64, i32, dbl, u64,
+                                          u64, u64, vp, vp]
+        L.sd_ref_accept_probs.restype = ctypes.c_int
         L.sd_ref_outcome_dist.argtypes = [vp, vp, vp, i32, i32, i32, i64, i64, i32, dbl, vp]
         L.sd_ref_outcome_dist.restype = ctypes.c_int
         L.sd_ref_beta.argtypes = [vp, vp, i32, dbl]
@@ -142,6 +145,23 @@ def sample_check(p, q, ids, b, L, t, T, seed=0, round=0, rid_base=0, V=None):
     if rc != 0:
         raise ValueError("sd_ref_sample_check: invalid argument")
     return tuple(o.value for o in out)
+
+
+def accept_probs(p, q, ids, b, T, seed=0, round=0, rid_base=0, V=None):
+    """(a_j, u_acc(j)) for every position j of request b (no early stop)."""
+    p, dt = _logits(p, "p")
+    q, _ = _logits(q, "q")
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    k = ids.shape[1]
+    V = p.shape[-1] if V is None else V
+    a = np.zeros(k)
+    u = np.zeros(k)
+    rc = lib().sd_ref_accept_probs(_ptr(p), _ptr(q), _ptr(ids), b, k, V, p.shape[-1],
+                                   q.shape[-1], dt, float(T), seed, round, rid_base, _ptr(a),
+                                   _ptr(u))
+    if rc != 0:
+        raise ValueError("sd_ref_accept_probs: invalid argument")
+    return a, u
 
 
 def outcome_dist(p, q, ids, T, V=None):

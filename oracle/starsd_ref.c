@@ -400,6 +400,30 @@ int sd_ref_sample_check(const void* p, const void* q, const int32_t* ids,
     return 0;
 }
 
+int sd_ref_accept_probs(const void* p, const void* q, const int32_t* ids,
+                        int32_t b, int32_t k, int32_t V, int64_t ld_p, int64_t ld_q, int32_t dtype,
+                        double T, uint64_t seed, uint64_t round, uint64_t rid_base,
+                        double* a_out, double* u_out) {
+    if (!p || !q || !ids || !(T > 0.0) || k < 1 || k > SD_REF_KMAX) return 1;
+    if (ld_p == 0) ld_p = V;
+    if (ld_q == 0) ld_q = V;
+    batch_t a = {p, q, ids, b + 1, k, V, ld_p, ld_q, dtype, T, seed, round, rid_base,
+                 NULL, NULL, NULL, NULL};
+    for (int32_t j = 0; j < k; ++j) {
+        int32_t x = ids[(size_t)b * k + j];
+        row_t pr = p_row(&a, b, j), qr = q_row(&a, b, j);
+        double lam_p = row_logsumexp(pr, T), lam_q = row_logsumexp(qr, T);
+        double zq = z_of(qr, x);
+        if (zq == -INFINITY) a_out[j] = 0.0;
+        else {
+            double ell = (z_of(pr, x) / T - lam_p) - (zq / T - lam_q);
+            a_out[j] = ell >= 0.0 ? 1.0 : exp(ell);
+        }
+        sd_ref_uniforms(seed, (uint32_t)j, round, rid_base + (uint64_t)b, &u_out[j], NULL);
+    }
+    return 0;
+}
+
 /* Exact distribution of (L, emitted token) for fixed draft paths, with the continuous
  * uniforms of P:730 integrated out:
  *   Pr(L = j, t = y) = (prod_{i<j} a_i) (1 - a_j) r_j(y) / R_j      (j < k)

@@ -77,6 +77,14 @@ int sd_ref_sample_check(const void* p, const void* q, const int32_t* ids,
                         double T, uint64_t seed, uint64_t round, uint64_t rid_base,
                         int32_t L, int32_t t, double* C_prev, double* C_tok, double* R, double* theta);
 
+/* a_j = min(1, p_j(x_j)/q_j(x_j)) and u_acc(j) at EVERY position j = 0..k-1 of request b
+ * (no early stop; rows assumed fault-free).  Used by the C-13 tie rule when a GPU result
+ * stops at a different position than the oracle. */
+int sd_ref_accept_probs(const void* p, const void* q, const int32_t* ids,
+                        int32_t b, int32_t k, int32_t V, int64_t ld_p, int64_t ld_q, int32_t dtype,
+                        double T, uint64_t seed, uint64_t round, uint64_t rid_base,
+                        double* a_out, double* u_out);
+
 /* Exact outcome distribution of one verify call, integrating the uniforms analytically
  * (continuous U(0,1) of P:730):  out[b][j][y] = Pr(L = j, emitted token = y | draft path).
  * Shape [B][k+1][V], fp64.  Used by the exact-enumeration losslessness pins. */

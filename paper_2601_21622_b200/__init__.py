@@ -1,0 +1,151 @@
+"""paper_2601_21622_b200 -- B200-native StarSD verify path (arXiv 2601.21622).
+
+Thin Python binding over libstarsd.so (include/starsd.h).  This module only marshals torch
+tensors into the C ABI (pointers, shapes, the current CUDA stream); every step of the verify
+path runs in the sm_100a kernels.  PyTorch provides device memory and streams, nothing else.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import StarsdError, check
+
+__all__ = ["verify", "verify_host", "workspace_size", "philox_words", "Workspace", "StarsdError",
+           "version"]
+
+FAULT_BAD_DRAFT_ID, FAULT_NONFINITE, FAULT_EMPTY_ROW = 1, 2, 4
+FAULT_ZERO_Q, FAULT_ZERO_RESIDUAL = 8, 16
+
+
+def version() -> str:
+    return _lib.load().sd_version().decode()
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return _lib.SD_DTYPE_F32
+    if t.dtype == torch.bfloat16:
+        return _lib.SD_DTYPE_BF16
+    raise TypeError(f"logits must be float32 or bfloat16, got {t.dtype}")
+
+
+def _shape(batch, k, vocab, ld_p, ld_q, dtype_code) -> _lib.Shape:
+    return _lib.Shape(batch, k, vocab, ld_p, ld_q, dtype_code)
+
+
+def workspace_size(batch: int, k: int, vocab: int, temperature: float,
+                   dtype: torch.dtype = torch.float32) -> int:
+    code = _lib.SD_DTYPE_F32 if dtype == torch.float32 else _lib.SD_DTYPE_BF16
+    n = ctypes.c_size_t()
+    sh = _shape(batch, k, vocab, 0, 0, code)
+    check(_lib.load().sd_verify_workspace_size(ctypes.byref(sh), float(temperature),
+                                               ctypes.byref(n)), "sd_verify_workspace_size")
+    return n.value
+
+
+class Workspace:
+    """A zero-filled device workspace; sd_verify leaves it zero-filled after every call."""
+
+    def __init__(self, batch, k, vocab, temperature, dtype=torch.float32, device=None):
+        self.nbytes = workspace_size(batch, k, vocab, temperature, dtype)
+        self.buf = torch.zeros(max(self.nbytes, 16), dtype=torch.uint8, device=device)
+
+
+_ws_cache: dict = {}
+
+
+def _workspace_for(device, batch, k, vocab, temperature, dtype) -> Workspace:
+    key = (str(device), batch, k, vocab, temperature == 0.0, dtype)
+    ws = _ws_cache.get(key)
+    if ws is None:
+        ws = Workspace(batch, k, vocab, temperature, dtype, device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def verify(p: torch.Tensor, q: torch.Tensor | None, ids: torch.Tensor, temperature: float,
+           seed: int = 0, round: int = 0, request_id_base: int = 0, vocab: int | None = None,
+           out: tuple | None = None, workspace: Workspace | None = None,
+           stream: torch.cuda.Stream | None = None):
+    """One batched verify step (sd_verify).  p: [B, k+1, ld] and q: [B, k, ld] CUDA tensors
+    (float32 or bfloat16, rows contiguous), ids: [B, k] int32.  Returns (accept_len [B],
+    tokens [B, k+1], status [B]) int32 CUDA tensors, ordered on `stream` (default: current)."""
+    if not p.is_cuda:
+        raise StarsdError("verify(): tensors must be CUDA tensors (use verify_host for host data)")
+    B, k1, ld_p = p.shape
+    k = k1 - 1
+    if ids.shape != (B, k) or ids.dtype != torch.int32 or not ids.is_contiguous():
+        raise StarsdError("ids must be a contiguous int32 [B, k] tensor")
+    if p.stride(-1) != 1 or p.stride(-2) != ld_p or p.stride(0) != k1 * ld_p:
+        raise StarsdError("p must be contiguous [B, k+1, ld]")
+    code = _dtype_code(p)
+    ld_q = 0
+    qptr = None
+    if q is not None:
+        if q.dtype != p.dtype or q.shape[:2] != (B, k) or q.stride(-1) != 1:
+            raise StarsdError("q must be [B, k, ld] with the dtype of p")
+        ld_q = q.shape[-1]
+        if q.stride(-2) != ld_q or q.stride(0) != k * ld_q:
+            raise StarsdError("q must be contiguous [B, k, ld]")
+        qptr = q.data_ptr()
+    V = ld_p if vocab is None else vocab
+    if out is None:
+        L = torch.empty(B, dtype=torch.int32, device=p.device)
+        tok = torch.empty(B, k + 1, dtype=torch.int32, device=p.device)
+        st = torch.empty(B, dtype=torch.int32, device=p.device)
+    else:
+        L, tok, st = out
+    ws = workspace or _workspace_for(p.device, B, k, V, float(temperature), p.dtype)
+    sh = _shape(B, k, V, ld_p, ld_q, code)
+    s = stream if stream is not None else torch.cuda.current_stream(p.device)
+    check(_lib.load().sd_verify(p.data_ptr(), qptr, ids.data_ptr(), ctypes.byref(sh),
+                                float(temperature), seed & (2**64 - 1), round & (2**64 - 1),
+                                request_id_base & (2**64 - 1), L.data_ptr(), tok.data_ptr(),
+                                st.data_ptr() if st is not None else None, ws.buf.data_ptr(),
+                                ws.nbytes, s.cuda_stream), "sd_verify")
+    return L, tok, st
+
+
+def verify_host(p: torch.Tensor, q: torch.Tensor | None, ids: torch.Tensor, temperature: float,
+                seed: int = 0, round: int = 0, request_id_base: int = 0,
+                device: torch.device | str = "cuda", staging: dict | None = None):
+    """End-to-end call on HOST tensors (pinned for async copies): host->device copies of the
+    inputs, sd_verify, device->host copy of the results, then a stream synchronize.
+    `staging` (optional dict) caches the device buffers between calls."""
+    dev = torch.device(device)
+    st = staging if staging is not None else {}
+    if "p" not in st or st["p"].shape != p.shape or st["p"].dtype != p.dtype:
+        st["p"] = torch.empty(p.shape, dtype=p.dtype, device=dev)
+        st["q"] = torch.empty(q.shape, dtype=q.dtype, device=dev) if q is not None else None
+        st["ids"] = torch.empty(ids.shape, dtype=torch.int32, device=dev)
+        B, k = ids.shape
+        st["out"] = (torch.empty(B, dtype=torch.int32, device=dev),
+                     torch.empty(B, k + 1, dtype=torch.int32, device=dev),
+                     torch.empty(B, dtype=torch.int32, device=dev))
+        st["host_out"] = tuple(torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                               for t in st["out"])
+    st["p"].copy_(p, non_blocking=True)
+    if q is not None:
+        st["q"].copy_(q, non_blocking=True)
+    st["ids"].copy_(ids, non_blocking=True)
+    verify(st["p"], st["q"], st["ids"], temperature, seed, round, request_id_base,
+           out=st["out"])
+    for h, d in zip(st["host_out"], st["out"]):
+        h.copy_(d, non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
+    return st["host_out"]
+
+
+def philox_words(seed: int, round: int, pos: torch.Tensor, rid: torch.Tensor) -> torch.Tensor:
+    """The four Philox4x32-10 words per (pos, rid) the verify step draws from (CUDA tensors:
+    pos int32/uint32 [n], rid int64 [n]).  Returns int64 [n, 4] holding the uint32 words."""
+    n = pos.numel()
+    out = torch.empty(n, 4, dtype=torch.int32, device=pos.device)
+    s = torch.cuda.current_stream(pos.device)
+    check(_lib.load().sd_philox_uniforms(seed & (2**64 - 1), round & (2**64 - 1),
+                                         pos.contiguous().data_ptr(), rid.contiguous().data_ptr(),
+                                         n, out.data_ptr(), s.cuda_stream), "sd_philox_uniforms")
+    return out.to(torch.int64) & 0xFFFFFFFF

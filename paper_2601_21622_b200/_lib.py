@@ -1,0 +1,111 @@
+"""ctypes prototypes of include/starsd.h.  Loading fails loudly if libstarsd.so is missing:
+there is no CPU fallback anywhere on the product path."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libstarsd.so")
+
+SD_OK = 0
+STATUS_NAMES = {0: "SD_OK", 1: "SD_ERR_INVALID_ARGUMENT", 2: "SD_ERR_UNSUPPORTED",
+                3: "SD_ERR_CUDA", 4: "SD_ERR_NCCL", 5: "SD_ERR_TIMEOUT", 6: "SD_ERR_NOT_READY",
+                7: "SD_ERR_INTERNAL"}
+SD_DTYPE_F32, SD_DTYPE_BF16 = 0, 1
+STAR_ID_BYTES = 128
+
+# every symbol the header declares (tests check the library exports all of them)
+EXPORTS = ["sd_verify", "sd_verify_workspace_size", "sd_philox_uniforms", "sd_star_unique_ids",
+           "sd_star_create", "sd_star_round", "sd_star_poll", "sd_star_draft_begin",
+           "sd_star_draft_end", "sd_star_stats", "sd_star_destroy", "sd_status_string",
+           "sd_last_error", "sd_version", "sd_profile_events"]
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("k", ctypes.c_int32), ("vocab", ctypes.c_int32),
+                ("ld_p", ctypes.c_int64), ("ld_q", ctypes.c_int64), ("dtype", ctypes.c_int32)]
+
+
+class StarConfig(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("n_slots", ctypes.c_int32),
+                ("max_shape", Shape), ("temperature", ctypes.c_float), ("seed", ctypes.c_uint64),
+                ("timeout_ms", ctypes.c_int32), ("device", ctypes.c_int32)]
+
+
+class RoundDesc(ctypes.Structure):
+    _fields_ = [("verifier", ctypes.c_int32), ("slot", ctypes.c_int32), ("round", ctypes.c_uint64),
+                ("batch", ctypes.c_int32), ("request_id_base", ctypes.c_uint64),
+                ("p_logits", ctypes.c_void_p), ("draft_ids", ctypes.c_void_p),
+                ("q_logits", ctypes.c_void_p), ("out_accept_len", ctypes.c_void_p),
+                ("out_tokens", ctypes.c_void_p)]
+
+
+class StarStats(ctypes.Structure):
+    _fields_ = [("busy_fraction", ctypes.c_double), ("mean_idle_ms", ctypes.c_double),
+                ("mean_wait_ms", ctypes.c_double), ("window_ms", ctypes.c_double),
+                ("rounds", ctypes.c_uint64)]
+
+
+class StarsdError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load():
+    """Load libstarsd.so (built by paper_2601_21622_b200.build / __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise StarsdError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
+                          f"g.build()'` (the CUDA extension is required; there is no fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, u32, i64, u64, sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32,
+                                  ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t)
+    st = ctypes.c_int
+    L.sd_verify.argtypes = [vp, vp, vp, ctypes.POINTER(Shape), ctypes.c_float, u64, u64, u64,
+                            vp, vp, vp, vp, sz, vp]
+    L.sd_verify.restype = st
+    L.sd_verify_workspace_size.argtypes = [ctypes.POINTER(Shape), ctypes.c_float,
+                                           ctypes.POINTER(sz)]
+    L.sd_verify_workspace_size.restype = st
+    L.sd_philox_uniforms.argtypes = [u64, u64, vp, vp, i32, vp, vp]
+    L.sd_philox_uniforms.restype = st
+    L.sd_star_unique_ids.argtypes = [i32, vp]
+    L.sd_star_unique_ids.restype = st
+    L.sd_star_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(StarConfig), vp]
+    L.sd_star_create.restype = st
+    L.sd_star_round.argtypes = [vp, ctypes.POINTER(RoundDesc), vp]
+    L.sd_star_round.restype = st
+    L.sd_star_poll.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32),
+                               ctypes.POINTER(u64), i32]
+    L.sd_star_poll.restype = st
+    L.sd_star_draft_begin.argtypes = [vp, vp]
+    L.sd_star_draft_begin.restype = st
+    L.sd_star_draft_end.argtypes = [vp, vp]
+    L.sd_star_draft_end.restype = st
+    L.sd_star_stats.argtypes = [vp, ctypes.POINTER(StarStats)]
+    L.sd_star_stats.restype = st
+    L.sd_star_destroy.argtypes = [vp]
+    L.sd_star_destroy.restype = st
+    L.sd_profile_events.argtypes = [vp, i32]
+    L.sd_profile_events.restype = st
+    L.sd_status_string.argtypes = [st]
+    L.sd_status_string.restype = ctypes.c_char_p
+    L.sd_last_error.argtypes = []
+    L.sd_last_error.restype = ctypes.c_char_p
+    L.sd_version.argtypes = []
+    L.sd_version.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str):
+    if rc != SD_OK:
+        L = load()
+        raise StarsdError(f"{what}: {STATUS_NAMES.get(rc, rc)}: "
+                          f"{L.sd_last_error().decode(errors='replace')}")
+    return rc

@@ -1,0 +1,188 @@
+// abi.cu -- the extern "C" boundary of libstarsd.so (include/starsd.h): argument validation,
+// workspace layout, dispatch to the sm_100a kernels, status strings.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/starsd.h"
+#include "abi_internal.h"
+#include "verify.cuh"
+
+namespace sd {
+cudaError_t launch_verify(const Params& P, bool greedy, bool bf16, cudaStream_t st,
+                          cudaEvent_t ev0, cudaEvent_t ev1);
+cudaError_t launch_philox(uint64_t seed, uint64_t round, const uint32_t* pos, const uint64_t* rid,
+                          int n, uint32_t* out, cudaStream_t st);
+
+static thread_local char g_err[512] = "";
+static thread_local cudaEvent_t* g_prof_ev = nullptr;
+static thread_local int32_t g_prof_n = 0, g_prof_i = 0;
+
+sd_status fail(sd_status s, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return s;
+}
+void clear_error() { g_err[0] = '\0'; }
+const char* last_error() { return g_err; }
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Validate a shape + temperature; fills the element size.
+sd_status check_shape(const sd_shape* s, float T, int* esz) {
+    if (!s) return fail(SD_ERR_INVALID_ARGUMENT, "shape is NULL");
+    if (s->batch < 0) return fail(SD_ERR_INVALID_ARGUMENT, "shape.batch=%d < 0", s->batch);
+    if (s->k < 1 || s->k > SD_MAX_K)
+        return fail(SD_ERR_INVALID_ARGUMENT, "shape.k=%d outside [1, %d]", s->k, SD_MAX_K);
+    if (s->vocab < 2) return fail(SD_ERR_INVALID_ARGUMENT, "shape.vocab=%d < 2", s->vocab);
+    if (s->dtype != SD_DTYPE_F32 && s->dtype != SD_DTYPE_BF16)
+        return fail(SD_ERR_INVALID_ARGUMENT, "shape.dtype=%d unknown", (int)s->dtype);
+    *esz = s->dtype == SD_DTYPE_F32 ? 4 : 2;
+    const int64_t ldp = s->ld_p ? s->ld_p : s->vocab, ldq = s->ld_q ? s->ld_q : s->vocab;
+    if (ldp < s->vocab || ldq < s->vocab)
+        return fail(SD_ERR_INVALID_ARGUMENT, "row stride smaller than vocab");
+    if ((ldp * *esz) % 16 != 0 || (ldq * *esz) % 16 != 0)
+        return fail(SD_ERR_INVALID_ARGUMENT,
+                    "row strides must be multiples of 16 bytes (ld_p=%lld, ld_q=%lld)",
+                    (long long)ldp, (long long)ldq);
+    if (!(T == 0.0f || (std::isfinite(T) && T >= 1e-3f)))
+        return fail(SD_ERR_INVALID_ARGUMENT, "temperature=%g must be 0 or finite >= 1e-3",
+                    (double)T);
+    int32_t nch, CH;
+    chunking(s->vocab, *esz, &nch, &CH);
+    if (nch > 256)
+        return fail(SD_ERR_UNSUPPORTED, "vocab=%d too large for this build (max %d)", s->vocab,
+                    256 * (kMaxChunkBytes / *esz));
+    const int64_t grid = (int64_t)(s->k + 1) * s->batch * nch;
+    if (grid > 0x7FFFFFFFLL) return fail(SD_ERR_UNSUPPORTED, "batch too large");
+    return SD_OK;
+}
+
+}  // namespace sd
+
+using namespace sd;
+
+extern "C" {
+
+sd_status sd_verify_workspace_size(const sd_shape* shape, float temperature, size_t* bytes) {
+    clear_error();
+    int esz;
+    sd_status s = check_shape(shape, temperature, &esz);
+    if (s != SD_OK) return s;
+    if (!bytes) return fail(SD_ERR_INVALID_ARGUMENT, "bytes is NULL");
+    *bytes = ws_layout(shape->batch, shape->k, shape->vocab, esz).total;
+    return SD_OK;
+}
+
+sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* draft_ids,
+                    const sd_shape* shape, float temperature, uint64_t seed, uint64_t round,
+                    uint64_t request_id_base, int32_t* out_accept_len, int32_t* out_tokens,
+                    int32_t* out_status, void* workspace, size_t workspace_bytes,
+                    cudaStream_t stream) {
+    clear_error();
+    int esz;
+    sd_status s = check_shape(shape, temperature, &esz);
+    if (s != SD_OK) return s;
+    if (shape->batch == 0) return SD_OK;
+    const bool greedy = temperature == 0.0f;
+    if (!p_logits) return fail(SD_ERR_INVALID_ARGUMENT, "p_logits is NULL");
+    if (!greedy && !q_logits) return fail(SD_ERR_INVALID_ARGUMENT, "q_logits is NULL (T > 0)");
+    if (!draft_ids) return fail(SD_ERR_INVALID_ARGUMENT, "draft_ids is NULL");
+    if (!out_accept_len || !out_tokens)
+        return fail(SD_ERR_INVALID_ARGUMENT, "out_accept_len / out_tokens is NULL");
+    if (!workspace) return fail(SD_ERR_INVALID_ARGUMENT, "workspace is NULL");
+    if (!aligned16(p_logits) || (!greedy && !aligned16(q_logits)) || !aligned16(workspace))
+        return fail(SD_ERR_INVALID_ARGUMENT, "p_logits / q_logits / workspace not 16-byte aligned");
+    const WsLayout w = ws_layout(shape->batch, shape->k, shape->vocab, esz);
+    if (workspace_bytes < w.total)
+        return fail(SD_ERR_INVALID_ARGUMENT, "workspace_bytes=%zu < required %zu",
+                    workspace_bytes, w.total);
+
+    Params P{};
+    P.p = p_logits;
+    P.q = greedy ? nullptr : q_logits;
+    P.ids = draft_ids;
+    P.B = shape->batch;
+    P.k = shape->k;
+    P.V = shape->vocab;
+    P.ld_p = shape->ld_p ? shape->ld_p : shape->vocab;
+    P.ld_q = shape->ld_q ? shape->ld_q : shape->vocab;
+    chunking(P.V, esz, &P.nch, &P.CH);
+    P.nseg = P.CH / (32 * (kVecBytes / esz));
+    // c2 = log2(e) / T rounded to fp32; every exponent in the kernels uses this one constant
+    P.c2 = greedy ? 0.0f : static_cast<float>(1.4426950408889634 / static_cast<double>(temperature));
+    P.c2d = static_cast<double>(P.c2);
+    P.seed = seed;
+    P.round = round;
+    P.rid_base = request_id_base;
+    P.out_L = out_accept_len;
+    P.out_tok = out_tokens;
+    P.out_status = out_status;
+    char* ws = static_cast<char*>(workspace);
+    P.rej_mask = reinterpret_cast<uint32_t*>(ws + w.rej_mask);
+    P.ticketA = reinterpret_cast<uint32_t*>(ws + w.ticketA);
+    P.ticketB = reinterpret_cast<uint32_t*>(ws + w.ticketB);
+    P.rowstat = reinterpret_cast<RowStat*>(ws + w.rowstat);
+    P.partA = reinterpret_cast<PartA*>(ws + w.partA);
+    P.partB = reinterpret_cast<PartB*>(ws + w.partB);
+    P.segtab = reinterpret_cast<double2*>(ws + w.segtab);
+
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (g_prof_ev && g_prof_i < g_prof_n) {
+        ev0 = g_prof_ev[2 * g_prof_i];
+        ev1 = g_prof_ev[2 * g_prof_i + 1];
+        ++g_prof_i;
+    }
+    cudaError_t e = launch_verify(P, greedy, shape->dtype == SD_DTYPE_BF16, stream, ev0, ev1);
+    if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return SD_OK;
+}
+
+sd_status sd_philox_uniforms(uint64_t seed, uint64_t round, const uint32_t* pos,
+                             const uint64_t* rid, int32_t n, uint32_t* out_words,
+                             cudaStream_t stream) {
+    clear_error();
+    if (n < 0) return fail(SD_ERR_INVALID_ARGUMENT, "n < 0");
+    if (n > 0 && (!pos || !rid || !out_words))
+        return fail(SD_ERR_INVALID_ARGUMENT, "NULL pointer");
+    if (!aligned16(out_words)) return fail(SD_ERR_INVALID_ARGUMENT, "out_words not 16-byte aligned");
+    cudaError_t e = launch_philox(seed, round, pos, rid, n, out_words, stream);
+    if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return SD_OK;
+}
+
+sd_status sd_profile_events(cudaEvent_t* events, int32_t n_pairs) {
+    clear_error();
+    if (n_pairs < 0 || (n_pairs > 0 && !events))
+        return fail(SD_ERR_INVALID_ARGUMENT, "events / n_pairs");
+    g_prof_ev = n_pairs ? events : nullptr;
+    g_prof_n = n_pairs;
+    g_prof_i = 0;
+    return SD_OK;
+}
+
+const char* sd_status_string(sd_status s) {
+    switch (s) {
+        case SD_OK: return "SD_OK";
+        case SD_ERR_INVALID_ARGUMENT: return "SD_ERR_INVALID_ARGUMENT";
+        case SD_ERR_UNSUPPORTED: return "SD_ERR_UNSUPPORTED";
+        case SD_ERR_CUDA: return "SD_ERR_CUDA";
+        case SD_ERR_NCCL: return "SD_ERR_NCCL";
+        case SD_ERR_TIMEOUT: return "SD_ERR_TIMEOUT";
+        case SD_ERR_NOT_READY: return "SD_ERR_NOT_READY";
+        case SD_ERR_INTERNAL: return "SD_ERR_INTERNAL";
+    }
+    return "SD_ERR_UNKNOWN";
+}
+
+const char* sd_last_error(void) { return last_error(); }
+
+const char* sd_version(void) { return "starsd-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// verify.cuh -- internal layout shared by the verify kernels and the C-ABI dispatcher.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace sd {
+
+constexpr int kThreads = 256;            // threads per CTA (8 warps)
+constexpr int kWarps = kThreads / 32;
+constexpr int kVecBytes = 16;            // one 128-bit smem/global vector per thread per tile
+constexpr int kTileBytes = kThreads * kVecBytes;   // 4 KB of one row per tile
+constexpr int kMaxChunkBytes = 32 * 1024;          // one CTA owns <= 32 KB of a row
+
+// Per (request b, position j, vocab chunk c): what one kernel-A CTA found in its slice.
+struct PartA {
+    double S_p, S_q;     // sum over the slice of 2^((z - M_c) * c2), c2 = log2(e)/T (fp64 accum)
+    float M_p, M_q;      // slice max of the raw logits
+    float zx_p, zx_q;    // z_p,j(x_j), z_q,j(x_j) if x_j lies in this slice
+    int32_t flags;       // kPartNonfiniteP | kPartNonfiniteQ | kPartHasX
+    int32_t argmax;      // greedy: lowest index of the slice max (global token id)
+};
+constexpr int32_t kPartNonfiniteP = 1, kPartNonfiniteQ = 2, kPartHasX = 4;
+
+// Per (request b, position j): the whole-row statistics, written by the last kernel-A CTA of
+// that row pair, read by the sampling kernel.
+struct RowStat {
+    double S_p, S_q;     // row sums relative to the row max (same scale as PartA)
+    float M_p, M_q;      // row max
+    int32_t status;      // SD_FAULT_* bits decided at this position
+    int32_t argmax;      // greedy: argmax of p row (lowest index)
+};
+
+// Per (request b, chunk c) of the sampling pass.
+struct PartB {
+    double R;            // residual mass of the slice (or p mass at the bonus position)
+    double P;            // p mass of the slice (zero-residual fallback, C-6)
+};
+
+struct Params {
+    const void* p;
+    const void* q;
+    const int32_t* ids;
+    int32_t B, k, V;
+    int64_t ld_p, ld_q;          // elements
+    int32_t nch;                 // vocab chunks per row
+    int32_t CH;                  // elements per chunk (multiple of the tile)
+    float c2;                    // log2(e) / T   (fp32; sampled path)
+    double c2d;                  // the same value widened (exactly) to fp64
+    uint64_t seed, round, rid_base;
+    int32_t* out_L;
+    int32_t* out_tok;
+    int32_t* out_status;
+    // workspace (zero-filled region first)
+    uint32_t* rej_mask;          // [B]    bit j: position j rejected or faulted
+    uint32_t* ticketA;           // [B][k+1]
+    uint32_t* ticketB;           // [B]
+    RowStat* rowstat;            // [B][k+1]
+    PartA* partA;                // [B][k+1][nch]
+    PartB* partB;                // [B][nch]
+    double2* segtab;             // [B][nch][nseg]  (r mass, p mass) per warp segment
+    int32_t nseg;                // segments per chunk
+};
+
+// Workspace layout for a shape; all offsets 16-byte aligned.  The first `zero_bytes` must be
+// zero before a call and are zero again after it.
+struct WsLayout {
+    size_t rej_mask, ticketA, ticketB, zero_bytes;
+    size_t rowstat, partA, partB, segtab, total;
+};
+
+inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+inline void chunking(int32_t V, int32_t esz, int32_t* nch, int32_t* CH) {
+    const int64_t tile = kTileBytes / esz;                 // elements per tile
+    const int64_t chmax = kMaxChunkBytes / esz;
+    int64_t n = (V + chmax - 1) / chmax;
+    int64_t per = (V + n - 1) / n;
+    int64_t ch = (per + tile - 1) / tile * tile;
+    *nch = static_cast<int32_t>((V + ch - 1) / ch);
+    *CH = static_cast<int32_t>(ch);
+}
+
+inline WsLayout ws_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
+    int32_t nch, CH;
+    chunking(V, esz, &nch, &CH);
+    const int64_t nseg = CH / (32 * (kVecBytes / esz));
+    WsLayout w{};
+    size_t o = 0;
+    w.rej_mask = o; o = align16(o + sizeof(uint32_t) * B);
+    w.ticketA = o;  o = align16(o + sizeof(uint32_t) * (size_t)B * (k + 1));
+    w.ticketB = o;  o = align16(o + sizeof(uint32_t) * B);
+    w.zero_bytes = o;
+    w.rowstat = o;  o = align16(o + sizeof(RowStat) * (size_t)B * (k + 1));
+    w.partA = o;    o = align16(o + sizeof(PartA) * (size_t)B * (k + 1) * nch);
+    w.partB = o;    o = align16(o + sizeof(PartB) * (size_t)B * nch);
+    w.segtab = o;   o = align16(o + sizeof(double) * 2 * (size_t)B * nch * nseg);
+    w.total = o;
+    return w;
+}
+
+}  // namespace sd
