@@ -40,7 +40,9 @@ def workspace_size(batch: int, k: int, vocab: int, temperature: float,
                    dtype: torch.dtype = torch.float32) -> int:
     code = _lib.SD_DTYPE_F32 if dtype == torch.float32 else _lib.SD_DTYPE_BF16
     n = ctypes.c_size_t()
-    sh = _shape(batch, k, vocab, 0, 0, code)
+    per16 = 4 if code == _lib.SD_DTYPE_F32 else 8          # elements per 16 bytes
+    ld = (vocab + per16 - 1) // per16 * per16              # the size does not depend on ld
+    sh = _shape(batch, k, vocab, ld, ld, code)
     check(_lib.load().sd_verify_workspace_size(ctypes.byref(sh), float(temperature),
                                                ctypes.byref(n)), "sd_verify_workspace_size")
     return n.value

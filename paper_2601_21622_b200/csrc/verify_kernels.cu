@@ -712,9 +712,9 @@ static cudaError_t launch_sampled(const Params& P, cudaStream_t st, cudaEvent_t 
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_row_stats<E, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem > 48 * 1024 ? kMaxChunkBytes * 2 : smem));
+                             kMaxChunkBytes * 2);
         cudaFuncSetAttribute(k_sample<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem > 48 * 1024 ? kMaxChunkBytes * 2 : smem));
+                             kMaxChunkBytes * 2);
         attr = true;
     }
     const unsigned gridA = static_cast<unsigned>(P.k + 1) * P.B * P.nch;

@@ -22,7 +22,7 @@ def run_both(d, T, seed=1234, round=5, rid_base=1000, V=None, dtype=torch.float3
     def dev(a):
         if a is None:
             return None
-        t = torch.from_numpy(a)
+        t = torch.from_numpy(np.ascontiguousarray(a))
         if a.dtype == np.uint16:
             t = t.view(torch.bfloat16)
         return t.to(DEV)
