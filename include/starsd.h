@@ -134,6 +134,14 @@ sd_status sd_philox_uniforms(uint64_t seed, uint64_t round, const uint32_t* pos,
  */
 sd_status sd_profile_events(cudaEvent_t* events, int32_t n_pairs);
 
+/*
+ * sd_debug_trace -- development timeline.  When device_buf != NULL, subsequent sd_verify calls
+ * on this thread write %globaltimer stamps (ns) into it: [4 * grid] per-CTA start / producer
+ * phase-1 end / producer end / CTA exit, then [B*(k+1)] row-decision times, [B*(k+1)]
+ * sampling-pass end times, [B] request completion times.  NULL disables.
+ */
+sd_status sd_debug_trace(unsigned long long* device_buf);
+
 /* ======================================================================================
  * Star exchange + round scheduler (Alg. 1, Sec. 4.1, App. E)
  *

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/starsd.h"
@@ -15,12 +16,14 @@
 namespace sd {
 cudaError_t launch_verify(const Params& P, bool greedy, bool bf16, cudaStream_t st,
                           cudaEvent_t ev0, cudaEvent_t ev1);
+cudaError_t launch_fused(const fused::FParams& P, bool greedy, bool bf16, cudaStream_t st);
 cudaError_t launch_philox(uint64_t seed, uint64_t round, const uint32_t* pos, const uint64_t* rid,
                           int n, uint32_t* out, cudaStream_t st);
 
 static thread_local char g_err[512] = "";
 static thread_local cudaEvent_t* g_prof_ev = nullptr;
 static thread_local int32_t g_prof_n = 0, g_prof_i = 0;
+static thread_local unsigned long long* g_trace = nullptr;
 
 sd_status fail(sd_status s, const char* fmt, ...) {
     va_list ap;
@@ -31,6 +34,29 @@ sd_status fail(sd_status s, const char* fmt, ...) {
 }
 void clear_error() { g_err[0] = '\0'; }
 const char* last_error() { return g_err; }
+
+// STARSD_KERNEL=v1 selects the two-launch reference kernels (cross-variant checks);
+// the default is the single persistent fused kernel.
+static bool use_v1() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("STARSD_KERNEL");
+        v = (e && strcmp(e, "v1") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
+void record_event(cudaEvent_t ev, cudaStream_t st);
+
+// the fused kernel serves at most kFusedMaxBatch requests per launch; sd_verify splits larger
+// batches into consecutive launches on the same stream (the workspace is reused in order)
+constexpr int32_t kFusedMaxBatch = 4096;
+
+static size_t ws_bytes(int32_t B, int32_t k, int32_t V, int32_t esz) {
+    const int32_t Bl = B < kFusedMaxBatch ? B : kFusedMaxBatch;
+    const size_t a = ws_layout(B, k, V, esz).total, b = fused_layout(Bl, k, V, esz).total;
+    return a > b ? a : b;
+}
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -44,7 +70,8 @@ sd_status check_shape(const sd_shape* s, float T, int* esz) {
     if (s->dtype != SD_DTYPE_F32 && s->dtype != SD_DTYPE_BF16)
         return fail(SD_ERR_INVALID_ARGUMENT, "shape.dtype=%d unknown", (int)s->dtype);
     *esz = s->dtype == SD_DTYPE_F32 ? 4 : 2;
-    const int64_t ldp = s->ld_p ? s->ld_p : s->vocab, ldq = s->ld_q ? s->ld_q : s->vocab;
+    const int64_t ldp = s->ld_p ? s->ld_p : s->vocab;
+    const int64_t ldq = T == 0.0f ? ldp : (s->ld_q ? s->ld_q : s->vocab);   // q unused at T=0
     if (ldp < s->vocab || ldq < s->vocab)
         return fail(SD_ERR_INVALID_ARGUMENT, "row stride smaller than vocab");
     if ((ldp * *esz) % 16 != 0 || (ldq * *esz) % 16 != 0)
@@ -54,13 +81,11 @@ sd_status check_shape(const sd_shape* s, float T, int* esz) {
     if (!(T == 0.0f || (std::isfinite(T) && T >= 1e-3f)))
         return fail(SD_ERR_INVALID_ARGUMENT, "temperature=%g must be 0 or finite >= 1e-3",
                     (double)T);
-    int32_t nch, CH;
-    chunking(s->vocab, *esz, &nch, &CH);
-    if (nch > 256)
+    if (s->vocab > fused_max_vocab(*esz))
         return fail(SD_ERR_UNSUPPORTED, "vocab=%d too large for this build (max %d)", s->vocab,
-                    256 * (kMaxChunkBytes / *esz));
-    const int64_t grid = (int64_t)(s->k + 1) * s->batch * nch;
-    if (grid > 0x7FFFFFFFLL) return fail(SD_ERR_UNSUPPORTED, "batch too large");
+                    fused_max_vocab(*esz));
+    const int64_t rows = (int64_t)(s->k + 1) * s->batch;
+    if (rows >= (1LL << 31)) return fail(SD_ERR_UNSUPPORTED, "batch=%d too large", s->batch);
     return SD_OK;
 }
 
@@ -76,7 +101,7 @@ sd_status sd_verify_workspace_size(const sd_shape* shape, float temperature, siz
     sd_status s = check_shape(shape, temperature, &esz);
     if (s != SD_OK) return s;
     if (!bytes) return fail(SD_ERR_INVALID_ARGUMENT, "bytes is NULL");
-    *bytes = ws_layout(shape->batch, shape->k, shape->vocab, esz).total;
+    *bytes = ws_bytes(shape->batch, shape->k, shape->vocab, esz);
     return SD_OK;
 }
 
@@ -99,10 +124,79 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     if (!workspace) return fail(SD_ERR_INVALID_ARGUMENT, "workspace is NULL");
     if (!aligned16(p_logits) || (!greedy && !aligned16(q_logits)) || !aligned16(workspace))
         return fail(SD_ERR_INVALID_ARGUMENT, "p_logits / q_logits / workspace not 16-byte aligned");
-    const WsLayout w = ws_layout(shape->batch, shape->k, shape->vocab, esz);
-    if (workspace_bytes < w.total)
+    const size_t need = ws_bytes(shape->batch, shape->k, shape->vocab, esz);
+    if (workspace_bytes < need)
         return fail(SD_ERR_INVALID_ARGUMENT, "workspace_bytes=%zu < required %zu",
-                    workspace_bytes, w.total);
+                    workspace_bytes, need);
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (g_prof_ev && g_prof_i < g_prof_n) {
+        ev0 = g_prof_ev[2 * g_prof_i];
+        ev1 = g_prof_ev[2 * g_prof_i + 1];
+        ++g_prof_i;
+    }
+    // c2 = log2(e) / T rounded to fp32; every exponent in the kernels uses this one constant
+    const float c2 =
+        greedy ? 0.0f : static_cast<float>(1.4426950408889634 / static_cast<double>(temperature));
+    if (!use_v1()) {
+        const int32_t esz_ = esz;
+        for (int32_t off = 0; off < shape->batch; off += kFusedMaxBatch) {
+            const int32_t Bl = shape->batch - off < kFusedMaxBatch ? shape->batch - off : kFusedMaxBatch;
+            const FusedLayout w = fused_layout(Bl, shape->k, shape->vocab, esz_);
+            const int64_t ldp = shape->ld_p ? shape->ld_p : shape->vocab;
+            const int64_t ldq = shape->ld_q ? shape->ld_q : shape->vocab;
+            fused::FParams F{};
+            F.p = static_cast<const char*>(p_logits) + (size_t)off * (shape->k + 1) * ldp * esz_;
+            F.q = greedy ? nullptr
+                         : static_cast<const char*>(q_logits) + (size_t)off * shape->k * ldq * esz_;
+            F.ids = draft_ids + (size_t)off * shape->k;
+            F.B = Bl;
+            F.k = shape->k;
+            F.V = shape->vocab;
+            F.ld_p = ldp;
+            F.ld_q = ldq;
+            F.nch = w.nch;
+            F.CHI = w.CHI;
+            F.n_items = (shape->k + 1) * Bl * w.nch;
+            F.c2 = c2;
+            F.c2d = static_cast<double>(c2);
+            F.seed = seed;
+            F.round = round;
+            F.rid_base = request_id_base + static_cast<uint64_t>(off);
+            F.out_L = out_accept_len + off;
+            F.out_tok = out_tokens + (size_t)off * (shape->k + 1);
+            F.out_status = out_status ? out_status + off : nullptr;
+            char* ws = static_cast<char*>(workspace);
+            F.evt = reinterpret_cast<uint32_t*>(ws + w.evt);
+            F.stop = reinterpret_cast<uint32_t*>(ws + w.stop);
+            F.ticketA = reinterpret_cast<uint32_t*>(ws + w.ticketA);
+            F.ticketB = reinterpret_cast<uint32_t*>(ws + w.ticketB);
+            F.glob = reinterpret_cast<uint32_t*>(ws + w.glob);
+            F.mbox_tail = reinterpret_cast<uint32_t*>(ws + w.mbox_tail);
+            F.mbox = reinterpret_cast<uint32_t*>(ws + w.mbox);
+            F.mcap = w.mcap;
+            F.rowstat = reinterpret_cast<RowStat*>(ws + w.rowstat);
+            F.cand = reinterpret_cast<int2*>(ws + w.cand);
+            F.partA = reinterpret_cast<PartA*>(ws + w.partA);
+            F.partB = reinterpret_cast<PartB*>(ws + w.partB);
+            F.segtab = reinterpret_cast<double2*>(ws + w.segtab);
+            F.trace = g_trace;
+            {
+                static int dbg = -1;
+                if (dbg < 0) {
+                    const char* e = getenv("STARSD_DEBUG");
+                    dbg = e ? atoi(e) : 0;
+                }
+                F.debug = dbg;
+            }
+            if (off == 0) record_event(ev0, stream);
+            cudaError_t e = launch_fused(F, greedy, shape->dtype == SD_DTYPE_BF16, stream);
+            if (e != cudaSuccess)
+                return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+        }
+        record_event(ev1, stream);
+        return SD_OK;
+    }
+    const WsLayout w = ws_layout(shape->batch, shape->k, shape->vocab, esz);
 
     Params P{};
     P.p = p_logits;
@@ -115,8 +209,7 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     P.ld_q = shape->ld_q ? shape->ld_q : shape->vocab;
     chunking(P.V, esz, &P.nch, &P.CH);
     P.nseg = P.CH / (32 * (kVecBytes / esz));
-    // c2 = log2(e) / T rounded to fp32; every exponent in the kernels uses this one constant
-    P.c2 = greedy ? 0.0f : static_cast<float>(1.4426950408889634 / static_cast<double>(temperature));
+    P.c2 = c2;
     P.c2d = static_cast<double>(P.c2);
     P.seed = seed;
     P.round = round;
@@ -133,12 +226,6 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     P.partB = reinterpret_cast<PartB*>(ws + w.partB);
     P.segtab = reinterpret_cast<double2*>(ws + w.segtab);
 
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    if (g_prof_ev && g_prof_i < g_prof_n) {
-        ev0 = g_prof_ev[2 * g_prof_i];
-        ev1 = g_prof_ev[2 * g_prof_i + 1];
-        ++g_prof_i;
-    }
     cudaError_t e = launch_verify(P, greedy, shape->dtype == SD_DTYPE_BF16, stream, ev0, ev1);
     if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
     return SD_OK;
@@ -164,6 +251,11 @@ sd_status sd_profile_events(cudaEvent_t* events, int32_t n_pairs) {
     g_prof_ev = n_pairs ? events : nullptr;
     g_prof_n = n_pairs;
     g_prof_i = 0;
+    return SD_OK;
+}
+
+sd_status sd_debug_trace(unsigned long long* device_buf) {
+    g_trace = device_buf;
     return SD_OK;
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <vector_types.h>
 
 namespace sd {
 
@@ -97,5 +98,85 @@ inline WsLayout ws_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
     w.total = o;
     return w;
 }
+
+// ---- fused (v2) kernel: parameters and workspace layout ----------------------------------
+namespace fused {
+constexpr int kRowChunkBytesH = 16384;    // must equal fused::kRowChunkBytes in verify_fused.cu
+constexpr int kSegsH = 32;
+struct FParams {
+    const void* p;
+    const void* q;
+    const int32_t* ids;
+    int32_t B, k, V;
+    int64_t ld_p, ld_q;
+    int32_t nch, CHI;      // chunks per row, elements per chunk
+    int32_t n_items;       // (k+1) * B * nch phase-1 items
+    float c2;              // log2(e)/T in fp32
+    double c2d;            // the same value in fp64
+    uint64_t seed, round, rid_base;
+    int32_t* out_L;
+    int32_t* out_tok;
+    int32_t* out_status;
+    // zero-filled workspace region (left zero by every call)
+    uint32_t* evt;         // [B] rows_done | spawned << 8 | resid_done << 16
+    uint32_t* stop;        // [B] bit j: position j stops the chain (rejection or fault)
+    uint32_t* ticketA;     // [B*(k+1)] phase-1 chunk arrivals (skips in the high half)
+    uint32_t* ticketB;     // [B*(k+1)] phase-2 chunk arrivals
+    uint32_t* glob;        // [4] (unused), (unused), finished requests, exited CTAs
+    uint32_t* mbox_tail;   // [max grid] per-CTA mailbox fill counters
+    uint32_t* mbox;        // [max grid][mcap] per-CTA mailboxes of phase-2 work entries
+    int32_t mcap;
+    // scratch
+    RowStat* rowstat;      // [B*(k+1)]
+    int2* cand;            // [B*(k+1)] candidate token + informational status of a pass
+    PartA* partA;          // [B*(k+1)*nch]
+    PartB* partB;          // [B*(k+1)*nch]
+    double2* segtab;       // [B*(k+1)*nch*kSegs]
+    // optional debug timeline (nullptr in production): globaltimer stamps, see sd_debug_trace
+    unsigned long long* trace;
+    // development bisection knobs (0 in production): bit0 stream only (no requests complete;
+    // the kernel ends after phase 1), bit1 consumers skip the arithmetic, bit2 epilogue skips
+    // global traffic, bit3 producer ignores stop masks (no laziness)
+    int32_t debug;
+};
+
+}  // namespace fused
+
+constexpr int kFusedMaxGrid = 1024;
+constexpr int kFusedMinGrid = 64;
+
+struct FusedLayout {
+    size_t evt, stop, ticketA, ticketB, glob, mbox_tail, mbox, zero_bytes;
+    size_t rowstat, cand, partA, partB, segtab, total;
+    int32_t nch, CHI, mcap;
+};
+
+inline FusedLayout fused_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
+    FusedLayout w{};
+    w.CHI = fused::kRowChunkBytesH / esz;
+    w.nch = (V + w.CHI - 1) / w.CHI;
+    const size_t rows = static_cast<size_t>(B) * (k + 1);
+    // a sampling pass puts ceil(nch / grid) entries in each of min(nch, grid) mailboxes and
+    // every row sends at most one decider message; the kernel requires grid >= kFusedMinGrid
+    w.mcap = static_cast<int32_t>(rows * ((w.nch + kFusedMinGrid - 1) / kFusedMinGrid + 1));
+    size_t o = 0;
+    w.evt = o;     o = align16(o + 4 * (size_t)B);
+    w.stop = o;    o = align16(o + 4 * (size_t)B);
+    w.ticketA = o; o = align16(o + 4 * rows);
+    w.ticketB = o; o = align16(o + 4 * rows);
+    w.glob = o;    o = align16(o + 16);
+    w.mbox_tail = o; o = align16(o + 4 * (size_t)kFusedMaxGrid);
+    w.mbox = o;    o = align16(o + 4 * (size_t)kFusedMaxGrid * w.mcap);
+    w.zero_bytes = o;
+    w.rowstat = o; o = align16(o + sizeof(RowStat) * rows);
+    w.cand = o;    o = align16(o + 8 * rows);
+    w.partA = o;   o = align16(o + sizeof(PartA) * rows * w.nch);
+    w.partB = o;   o = align16(o + sizeof(PartB) * rows * w.nch);
+    w.segtab = o;  o = align16(o + 16 * rows * w.nch * fused::kSegsH);
+    w.total = o;
+    return w;
+}
+
+inline int fused_max_vocab(int32_t esz) { return 255 * (fused::kRowChunkBytesH / esz); }
 
 }  // namespace sd

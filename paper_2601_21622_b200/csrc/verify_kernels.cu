@@ -696,7 +696,7 @@ __global__ void k_philox(uint64_t seed, uint64_t round, const uint32_t* pos, con
 
 // Profiling event: a real timestamp record even while the stream is being captured into a
 // CUDA graph (external event node), a plain record otherwise.
-static void record_event(cudaEvent_t ev, cudaStream_t st) {
+void record_event(cudaEvent_t ev, cudaStream_t st) {
     if (!ev) return;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cs);

@@ -70,7 +70,7 @@ def test_workspace_size_is_host_only(lib):
     n = ctypes.c_size_t()
     s = shape(B=128, k=7, V=128256)
     assert lib.sd_verify_workspace_size(ctypes.byref(s), 1.0, ctypes.byref(n)) == 0
-    assert 0 < n.value < 16 * 1024 * 1024
+    assert 0 < n.value < 64 * 1024 * 1024
     assert n.value % 16 == 0
 
 
