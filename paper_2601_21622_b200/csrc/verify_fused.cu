@@ -1,4 +1,6 @@
-// verify_fused.cu -- the production sm_100a verify kernel: ONE persistent launch per call.
+// verify_fused.cu -- alternative sm_100a verify kernel: ONE persistent launch per call
+// (selected with STARSD_KERNEL=fused; the default two-launch path in verify_kernels.cu measured
+// faster on every BASELINE config -- see DESIGN.md "Kernel variants").
 //
 // Method (Alg. 2, readings C-1..C-12 of DESIGN.md), per request b:
 //   accept x_j iff u_acc(j) < min(1, p_j(x_j)/q_j(x_j)); L = first rejection (else k);

@@ -87,6 +87,16 @@ __device__ __forceinline__ T load_cg(const T* p) {
     return out;
 }
 
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+    float d;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ float warp_max_nan(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax_nan(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+    return v;
+}
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
@@ -137,7 +147,7 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
     __shared__ __align__(8) uint64_t bar;
     __shared__ int s_flag;
     __shared__ float s_mp[kWarps], s_mq[kWarps];
-    __shared__ int s_gi[kWarps], s_bad[kWarps];
+    __shared__ int s_gi[kWarps];
     __shared__ double s_sp[kWarps], s_sq[kWarps];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -192,54 +202,73 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
     __syncthreads();
     mbar_wait(&bar, 0);
 
-    // ---- sweep 1: slice max (greedy: + lowest argmax), non-finite check ------------------
-    float mp = -INFINITY, mq = -INFINITY;
+    // ---- sweep 1: slice max (NaN-propagating: a NaN makes the max NaN, +inf makes it +inf,
+    // so faults need no per-element test); greedy: lowest argmax + NaN-propagating max ------
+    const int nvec = len / VEC;                  // fully valid vectors
+    const bool tail = nvec * VEC < len;          // a ragged last vector (row end only)
+    const int tail_tid = nvec % kThreads;
+    float mp = -INFINITY, mq = -INFINITY, np = -INFINITY;
     int gi = INT_MAX;
-    bool badp = false, badq = false;
-    for (int e0 = tid * VEC; e0 < len; e0 += TILE) {
+#pragma unroll 4
+    for (int g = tid; g < nvec; g += kThreads) {
         float v[VEC];
-        EL::unpack(*reinterpret_cast<const uint4*>(sp + e0), v);
+        EL::unpack(*reinterpret_cast<const uint4*>(sp + g * VEC), v);
+        if (GREEDY) {
 #pragma unroll
+            for (int u = 0; u < VEC; ++u) {
+                np = fmax_nan(np, v[u]);
+                if (v[u] > mp) {
+                    mp = v[u];
+                    gi = c0 + g * VEC + u;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < VEC; u += 2) mp = fmax_nan(mp, fmax_nan(v[u], v[u + 1]));
+            if (load_q) {
+                EL::unpack(*reinterpret_cast<const uint4*>(sq + g * VEC), v);
+#pragma unroll
+                for (int u = 0; u < VEC; u += 2) mq = fmax_nan(mq, fmax_nan(v[u], v[u + 1]));
+            }
+        }
+    }
+    if (tail && tid == tail_tid) {
+        float v[VEC];
+        EL::unpack(*reinterpret_cast<const uint4*>(sp + nvec * VEC), v);
         for (int u = 0; u < VEC; ++u) {
-            if (e0 + u < len) {
-                badp |= nonfinite_or_nan(v[u]);
+            if (nvec * VEC + u < len) {
                 if (GREEDY) {
+                    np = fmax_nan(np, v[u]);
                     if (v[u] > mp) {
                         mp = v[u];
-                        gi = c0 + e0 + u;
+                        gi = c0 + nvec * VEC + u;
                     }
                 } else {
-                    mp = fmaxf(mp, v[u]);
+                    mp = fmax_nan(mp, v[u]);
                 }
             }
         }
         if (load_q) {
-            EL::unpack(*reinterpret_cast<const uint4*>(sq + e0), v);
-#pragma unroll
-            for (int u = 0; u < VEC; ++u) {
-                if (e0 + u < len) {
-                    badq |= nonfinite_or_nan(v[u]);
-                    mq = fmaxf(mq, v[u]);
-                }
-            }
+            EL::unpack(*reinterpret_cast<const uint4*>(sq + nvec * VEC), v);
+            for (int u = 0; u < VEC; ++u)
+                if (nvec * VEC + u < len) mq = fmax_nan(mq, v[u]);
         }
     }
     if (GREEDY) {
         warp_argmax(mp, gi);
+        np = warp_max_nan(np);
     } else {
-        mp = warp_max(mp);
-        mq = warp_max(mq);
+        mp = warp_max_nan(mp);
+        mq = warp_max_nan(mq);
     }
-    const unsigned bp = __ballot_sync(0xFFFFFFFFu, badp), bq = __ballot_sync(0xFFFFFFFFu, badq);
     if (lane == 0) {
         s_mp[warp] = mp;
-        s_mq[warp] = mq;
+        s_mq[warp] = GREEDY ? np : mq;
         s_gi[warp] = gi;
-        s_bad[warp] = (bp ? kPartNonfiniteP : 0) | (bq ? kPartNonfiniteQ : 0);
     }
     __syncthreads();
     float Mp = s_mp[0], Mq = s_mq[0];
-    int G = s_gi[0], bad = s_bad[0];
+    int G = s_gi[0];
 #pragma unroll
     for (int w = 1; w < kWarps; ++w) {
         if (GREEDY) {
@@ -247,36 +276,70 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
                 Mp = s_mp[w];
                 G = s_gi[w];
             }
+            Mq = fmax_nan(Mq, s_mq[w]);       // greedy: NaN-propagating max of p
         } else {
-            Mp = fmaxf(Mp, s_mp[w]);
-            Mq = fmaxf(Mq, s_mq[w]);
+            Mp = fmax_nan(Mp, s_mp[w]);
+            Mq = fmax_nan(Mq, s_mq[w]);
         }
-        bad |= s_bad[w];
+    }
+    int bad = 0;
+    if (GREEDY) {
+        bad = (Mq != Mq || Mq == INFINITY) ? kPartNonfiniteP : 0;
+        Mq = -INFINITY;
+    } else {
+        bad = ((Mp != Mp || Mp == INFINITY) ? kPartNonfiniteP : 0) |
+              ((Mq != Mq || Mq == INFINITY) ? kPartNonfiniteQ : 0);
     }
 
-    // ---- sweep 2: sum of 2^((z - M) c2), fp64 accumulation (one MUFU.EX2 per element) ----
+    // ---- sweep 2: sum of 2^((z - M) c2) against the CTA max (one MUFU.EX2 per element;
+    // fp32 within a vector, fp64 across vectors) ----------------------------------------------
     double Sp = 0.0, Sq = 0.0;
     if (!GREEDY) {
         const float c2 = P.c2;
         const bool okp = Mp > -INFINITY && Mp < INFINITY;
         const bool okq = load_q && Mq > -INFINITY && Mq < INFINITY;
-        for (int e0 = tid * VEC; e0 < len; e0 += TILE) {
-            float v[VEC];
-            if (okp) {
-                EL::unpack(*reinterpret_cast<const uint4*>(sp + e0), v);
-                float s = 0.0f;
+        const float ep = okp ? Mp : 0.0f, eq = okq ? Mq : 0.0f;
+        if (okp || okq) {
+#pragma unroll 4
+            for (int g = tid; g < nvec; g += kThreads) {
+                float v[VEC];
+                if (okp) {
+                    EL::unpack(*reinterpret_cast<const uint4*>(sp + g * VEC), v);
+                    float a0 = 0.0f, a1 = 0.0f;
 #pragma unroll
-                for (int u = 0; u < VEC; ++u)
-                    if (e0 + u < len) s += ex2_approx(__fmul_rn(__fsub_rn(v[u], Mp), c2));
-                Sp += static_cast<double>(s);
+                    for (int u = 0; u < VEC; u += 2) {
+                        a0 += ex2_approx(__fmul_rn(__fsub_rn(v[u], ep), c2));
+                        a1 += ex2_approx(__fmul_rn(__fsub_rn(v[u + 1], ep), c2));
+                    }
+                    Sp += static_cast<double>(a0 + a1);
+                }
+                if (okq) {
+                    EL::unpack(*reinterpret_cast<const uint4*>(sq + g * VEC), v);
+                    float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+                    for (int u = 0; u < VEC; u += 2) {
+                        a0 += ex2_approx(__fmul_rn(__fsub_rn(v[u], eq), c2));
+                        a1 += ex2_approx(__fmul_rn(__fsub_rn(v[u + 1], eq), c2));
+                    }
+                    Sq += static_cast<double>(a0 + a1);
+                }
             }
-            if (okq) {
-                EL::unpack(*reinterpret_cast<const uint4*>(sq + e0), v);
-                float s = 0.0f;
-#pragma unroll
-                for (int u = 0; u < VEC; ++u)
-                    if (e0 + u < len) s += ex2_approx(__fmul_rn(__fsub_rn(v[u], Mq), c2));
-                Sq += static_cast<double>(s);
+            if (tail && tid == tail_tid) {
+                float v[VEC];
+                if (okp) {
+                    EL::unpack(*reinterpret_cast<const uint4*>(sp + nvec * VEC), v);
+                    float t = 0.0f;
+                    for (int u = 0; u < VEC; ++u)
+                        if (nvec * VEC + u < len) t += ex2_approx(__fmul_rn(__fsub_rn(v[u], ep), c2));
+                    Sp += static_cast<double>(t);
+                }
+                if (okq) {
+                    EL::unpack(*reinterpret_cast<const uint4*>(sq + nvec * VEC), v);
+                    float t = 0.0f;
+                    for (int u = 0; u < VEC; ++u)
+                        if (nvec * VEC + u < len) t += ex2_approx(__fmul_rn(__fsub_rn(v[u], eq), c2));
+                    Sq += static_cast<double>(t);
+                }
             }
         }
         Sp = warp_sum(Sp);
@@ -341,15 +404,15 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
                 RG = a.argmax;
             }
         } else {
-            RMp = fmaxf(RMp, a.M_p);
-            RMq = fmaxf(RMq, a.M_q);
+            RMp = fmax_nan(RMp, a.M_p);
+            RMq = fmax_nan(RMq, a.M_q);
         }
     }
     if (GREEDY) {
         warp_argmax(RMp, RG);
     } else {
-        RMp = warp_max(RMp);
-        RMq = warp_max(RMq);
+        RMp = warp_max_nan(RMp);
+        RMq = warp_max_nan(RMq);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) flags |= __shfl_xor_sync(0xFFFFFFFFu, flags, o);
@@ -364,9 +427,9 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
         // rescale each slice sum from its own max to the row max: S_c * 2^((M_c - M) c2)
         for (int cc = lane; cc < nch; cc += 32) {
             const PartA a = load_cg(parts + cc);
-            if (a.S_p > 0.0)
+            if (a.S_p > 0.0 && RMp < INFINITY)
                 RSp += a.S_p * exp2((static_cast<double>(a.M_p) - RMp) * P.c2d);
-            if (a.S_q > 0.0)
+            if (a.S_q > 0.0 && RMq < INFINITY)
                 RSq += a.S_q * exp2((static_cast<double>(a.M_q) - RMq) * P.c2d);
         }
         RSp = warp_sum(RSp);
@@ -378,11 +441,11 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
     bool stop = false;
     if (j < kk && (x < 0 || x >= P.V)) st = kBadId;
     if (!st) {
-        if (flags & kPartNonfiniteP) st = kNonfinite;
+        if ((flags & kPartNonfiniteP) || !(RMp < INFINITY)) st = kNonfinite;
         else if (RMp == -INFINITY) st = kEmptyRow;
     }
     if (!st && load_q) {
-        if (flags & kPartNonfiniteQ) st = kNonfinite;
+        if ((flags & kPartNonfiniteQ) || !(RMq < INFINITY)) st = kNonfinite;
         else if (RMq == -INFINITY) st = kEmptyRow;
     }
     if (st) {
@@ -433,6 +496,9 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nch = P.nch, kk = P.k;
     const int c = blockIdx.x % nch, b = blockIdx.x / nch;
+    // programmatic dependent launch: this grid may start while k_row_stats drains; wait until
+    // every row decision of the primary grid is complete and visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint32_t mask = P.rej_mask[b];
     const int L = mask ? __ffs(mask) - 1 : kk;
     const RowStat rs = P.rowstat[static_cast<size_t>(b) * (kk + 1) + L];
@@ -473,14 +539,21 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
         __syncthreads();
         mbar_wait(&bar, 0);
 
-        const int ntile = P.CH / TILE;
-        for (int i = 0; i < ntile; ++i) {
-            const int e0 = i * TILE + tid * VEC;
-            double r4 = 0.0, p4 = 0.0;
-            if (e0 < len) {
+        // warp w computes segments w*PER .. w*PER+PER-1 of the chunk (SEG contiguous tokens
+        // each); PER <= 4 independent Kogge-Stone scans run interleaved.  Segment totals are
+        // the scans' last lanes -- the same routine the final search re-runs on one segment.
+        const int PER = nseg / kWarps;
+        double vr[4], vpm[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            vr[i] = 0.0;
+            vpm[i] = 0.0;
+            const int e0 = (warp * PER + i) * SEG + lane * VEC;
+            if (i < PER && e0 < len) {
                 float vp[VEC], vq[VEC];
                 EL::unpack(*reinterpret_cast<const uint4*>(sp + e0), vp);
                 if (use_q) EL::unpack(*reinterpret_cast<const uint4*>(sq + e0), vq);
+                double r4 = 0.0, p4 = 0.0;
 #pragma unroll
                 for (int u = 0; u < VEC; ++u) {
                     if (e0 + u < len) {
@@ -494,10 +567,26 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
                         p4 = __dadd_rn(p4, pd);
                     }
                 }
+                vr[i] = r4;
+                vpm[i] = p4;
             }
-            r4 = warp_incl_scan(r4, lane);
-            p4 = warp_incl_scan(p4, lane);
-            if (lane == 31) s_seg[i * kWarps + warp] = make_double2(r4, p4);
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double nr = __shfl_up_sync(0xFFFFFFFFu, vr[i], o);
+                const double np = __shfl_up_sync(0xFFFFFFFFu, vpm[i], o);
+                if (lane >= o) {
+                    vr[i] = __dadd_rn(vr[i], nr);
+                    vpm[i] = __dadd_rn(vpm[i], np);
+                }
+            }
+        }
+        if (lane == 31) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (i < PER) s_seg[warp * PER + i] = make_double2(vr[i], vpm[i]);
         }
         __syncthreads();
         double2* gseg = P.segtab + (static_cast<size_t>(b) * nch + c) * nseg;
@@ -664,6 +753,7 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
 // ------------------------------------------------------------------------------------------
 // Greedy finalize: one thread per request
 __global__ void k_finalize_greedy(const Params P) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= P.B) return;
     const int kk = P.k;
@@ -694,6 +784,24 @@ __global__ void k_philox(uint64_t seed, uint64_t round, const uint32_t* pos, con
 // ------------------------------------------------------------------------------------------
 // launchers (called from abi.cu)
 
+// Second kernel of a call: programmatic dependent launch, so its launch and prologue overlap the
+// tail of k_row_stats (the kernel waits with griddepcontrol.wait before reading decisions).
+template <typename K>
+static cudaError_t launch_dependent(K kernel, unsigned grid, unsigned block, size_t smem,
+                                    cudaStream_t st, const Params& P) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, P);
+}
+
 // Profiling event: a real timestamp record even while the stream is being captured into a
 // CUDA graph (external event node), a plain record otherwise.
 void record_event(cudaEvent_t ev, cudaStream_t st) {
@@ -715,14 +823,16 @@ static cudaError_t launch_sampled(const Params& P, cudaStream_t st, cudaEvent_t 
                              kMaxChunkBytes * 2);
         cudaFuncSetAttribute(k_sample<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kMaxChunkBytes * 2);
+
         attr = true;
     }
     const unsigned gridA = static_cast<unsigned>(P.k + 1) * P.B * P.nch;
     record_event(ev0, st);
     k_row_stats<E, false><<<gridA, kThreads, smem, st>>>(P);
     record_event(ev1, st);
-    k_sample<E><<<static_cast<unsigned>(P.B) * P.nch, kThreads, smem, st>>>(P);
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_dependent(k_sample<E>, static_cast<unsigned>(P.B) * P.nch, kThreads, smem, st, P);
 }
 
 template <typename E>
@@ -739,8 +849,9 @@ static cudaError_t launch_greedy(const Params& P, cudaStream_t st, cudaEvent_t e
     record_event(ev0, st);
     k_row_stats<E, true><<<gridA, kThreads, smem, st>>>(P);
     record_event(ev1, st);
-    k_finalize_greedy<<<(P.B + 127) / 128, 128, 0, st>>>(P);
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_dependent(k_finalize_greedy, (P.B + 127) / 128, 128, 0, st, P);
 }
 
 cudaError_t launch_verify(const Params& P, bool greedy, bool bf16, cudaStream_t st,
