@@ -222,6 +222,7 @@ def run_ours(args):
 
     import paper_2601_21622_b200 as sd
     from paper_2601_21622_b200 import _lib
+    from paper_2601_21622_b200.dp import reduce_max_sum, request_id_base
     from workload import make_batch_torch
 
     rank, world, local = dist_env()
@@ -242,7 +243,7 @@ def run_ours(args):
     tok_all = torch.empty(K, B, k + 1, dtype=torch.int32, device=dev)
     st_all = torch.empty(K, B, dtype=torch.int32, device=dev)
     ws = sd.Workspace(B, k, V, T, batches[0]["p"].dtype, dev)
-    rid0 = rank << 32
+    rid0 = request_id_base(rank)
 
     def step(i, out):
         bt = batches[i % args.nbatch]
@@ -295,15 +296,7 @@ def run_ours(args):
     ok = (sth & 7) == 0
     tokens = int((Lh + 1)[ok].sum())
     alg = float(algorithmic_bytes(Lh, V, k, e, greedy).sum())
-    stats = torch.tensor([ms, tokens, alg, sum(kA)], dtype=torch.float64, device=dev)
-    if world > 1:
-        mx = stats.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(stats, op=dist.ReduceOp.SUM)
-        ms_max = float(mx[0])
-    else:
-        ms_max = float(stats[0])
-    tokens_all = float(stats[1])
+    (ms_max,), (tokens_all,) = reduce_max_sum([ms], [tokens], dev)
     value = tokens_all / (ms_max / 1000.0)
 
     # dominant kernel (k_row_stats): algorithmic bytes of the whole step per launch / its time
@@ -349,15 +342,10 @@ def run_ours(args):
         s1.record()
         torch.cuda.synchronize()
         ems = s0.elapsed_time(s1)
-        es = torch.tensor([ems, etok], dtype=torch.float64, device=dev)
-        if world > 1:
-            emx = es.clone()
-            dist.all_reduce(emx, op=dist.ReduceOp.MAX)
-            dist.all_reduce(es, op=dist.ReduceOp.SUM)
-            ems = float(emx[0])
+        (ems,), (etok_all,) = reduce_max_sum([ems], [etok], dev)
         h2d = sum(t.numel() * t.element_size() for t in hb[0].values() if t is not None)
         d2h = B * 4 + B * (k + 1) * 4 + B * 4
-        e2e = {"value": float(es[1]) / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+        e2e = {"value": etok_all / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": E}
 
     cpu = None

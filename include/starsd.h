@@ -166,7 +166,13 @@ typedef struct {
     uint64_t seed;       /* Philox key used by the verifiers                                 */
     int32_t timeout_ms;  /* per-round completion timeout before SD_ERR_TIMEOUT (0 = none)    */
     int32_t device;      /* CUDA device ordinal of this rank                                 */
+    int32_t transport;   /* SD_STAR_NCCL, or SD_STAR_LOOPBACK: one process plays the draft and
+                            all world-1 verifiers on one device; the exchange is a D2D copy on
+                            the pair's stream and the draft's round desc carries p_logits.
+                            Same scheduler, poll and stats code as the NCCL transport.       */
 } sd_star_config;
+
+enum { SD_STAR_NCCL = 0, SD_STAR_LOOPBACK = 1 };
 
 /* One round for one (verifier, slot). */
 typedef struct {
@@ -175,7 +181,8 @@ typedef struct {
     uint64_t round;              /* Philox round selector                                        */
     int32_t batch;               /* B_v <= max_shape.batch                                       */
     uint64_t request_id_base;    /* Philox request-id base of this cohort                        */
-    const void* p_logits;        /* verifier: [B_v][k+1][V] target logits; draft: NULL           */
+    const void* p_logits;        /* verifier: [B_v][k+1][V] target logits; draft: NULL (NCCL) or
+                                    the virtual verifier's target logits (SD_STAR_LOOPBACK)      */
     const int32_t* draft_ids;    /* draft: send source [B_v][k]; verifier: NULL -> receive       */
     const void* q_logits;        /* draft: send source [B_v][k][V]; verifier: NULL -> receive    */
     int32_t* out_accept_len;     /* draft: receive dst [B_v]; verifier: local result [B_v]       */
@@ -184,7 +191,8 @@ typedef struct {
 
 typedef struct {
     double busy_fraction;   /* union of draft-busy intervals / window (M_q load)          */
-    double mean_idle_ms;    /* mean draft idle gap between busy intervals (T_idle, Eq. 9)        */
+    double mean_idle_ms;    /* total draft idle / number of consecutive-service pairs; with N
+                               verifiers served round-robin, N * mean_idle_ms = T_idle (Eq. 9)   */
     double mean_wait_ms;    /* mean time a completed return waited in Q_in before service        */
     double window_ms;       /* measurement window                                                */
     uint64_t rounds;        /* completed (verifier, slot) rounds                                 */
@@ -221,6 +229,19 @@ sd_status sd_star_draft_end(sd_star* h, cudaStream_t stream);
 
 sd_status sd_star_stats(sd_star* h, sd_star_stats_t* out);
 sd_status sd_star_destroy(sd_star* h);
+
+/*
+ * sd_star_simulate -- host-only run of the SAME work-conserving FIFO scheduler the draft rank
+ * uses, driven by a deterministic fake transport (no GPU, no NCCL): n_verifiers targets, each
+ * with n_slots independent closed-loop request streams (a stream issues its next request
+ * only after its previous one was verified); every draft service takes service_ms (S(d), Eq. 5)
+ * and every return takes return_ms (Z(d) = t_c + t_v, Eq. 6).  Runs `rounds` services and
+ * reports busy fraction, mean idle gap (T_idle, Eq. 9) and mean queueing wait (T_wait).
+ * For n_slots = 1 the busy fraction equals N S / (N S + T_idle) with
+ * T_idle = max(0, Z - (N - 1) S)  (Eqs. 8-10); the smallest N with no idle gap is ceil(Z/S)+1.
+ */
+sd_status sd_star_simulate(int32_t n_verifiers, int32_t n_slots, double service_ms,
+                           double return_ms, int32_t rounds, sd_star_stats_t* out);
 
 /* Static description of a status code. */
 const char* sd_status_string(sd_status s);

@@ -13,13 +13,16 @@ STATUS_NAMES = {0: "SD_OK", 1: "SD_ERR_INVALID_ARGUMENT", 2: "SD_ERR_UNSUPPORTED
                 3: "SD_ERR_CUDA", 4: "SD_ERR_NCCL", 5: "SD_ERR_TIMEOUT", 6: "SD_ERR_NOT_READY",
                 7: "SD_ERR_INTERNAL"}
 SD_DTYPE_F32, SD_DTYPE_BF16 = 0, 1
+SD_ERR_TIMEOUT, SD_ERR_NOT_READY = 5, 6
+SD_STAR_ID_BYTES = 128
 STAR_ID_BYTES = 128
 
 # every symbol the header declares (tests check the library exports all of them)
 EXPORTS = ["sd_verify", "sd_verify_workspace_size", "sd_philox_uniforms", "sd_star_unique_ids",
            "sd_star_create", "sd_star_round", "sd_star_poll", "sd_star_draft_begin",
            "sd_star_draft_end", "sd_star_stats", "sd_star_destroy", "sd_status_string",
-           "sd_last_error", "sd_version", "sd_profile_events", "sd_debug_trace"]
+           "sd_last_error", "sd_version", "sd_profile_events", "sd_debug_trace",
+           "sd_star_simulate"]
 
 
 class Shape(ctypes.Structure):
@@ -30,7 +33,11 @@ class Shape(ctypes.Structure):
 class StarConfig(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("n_slots", ctypes.c_int32),
                 ("max_shape", Shape), ("temperature", ctypes.c_float), ("seed", ctypes.c_uint64),
-                ("timeout_ms", ctypes.c_int32), ("device", ctypes.c_int32)]
+                ("timeout_ms", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("transport", ctypes.c_int32)]
+
+
+SD_STAR_NCCL, SD_STAR_LOOPBACK = 0, 1
 
 
 class RoundDesc(ctypes.Structure):
@@ -91,6 +98,9 @@ def load():
     L.sd_star_stats.restype = st
     L.sd_star_destroy.argtypes = [vp]
     L.sd_star_destroy.restype = st
+    L.sd_star_simulate.argtypes = [i32, i32, ctypes.c_double, ctypes.c_double, i32,
+                                   ctypes.POINTER(StarStats)]
+    L.sd_star_simulate.restype = st
     L.sd_profile_events.argtypes = [vp, i32]
     L.sd_profile_events.restype = st
     L.sd_debug_trace.argtypes = [vp]

@@ -1,0 +1,85 @@
+"""Star exchange + round scheduler on one GPU through the C ABI, using the
+loopback transport: one process plays the draft and N virtual verifiers, the exchange is a
+device copy on each pair's stream, and every round's results are checked against the oracle
+(DESIGN.md "Parity").  The NCCL transport shares the scheduler, poll and stats code; it needs
+two GPUs and is exercised by tools/star_demo.py under torchrun."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from parity import compare
+from workload import make_batch
+
+pytestmark = pytest.mark.gpu
+
+star = pytest.importorskip("paper_2601_21622_b200.star")
+DEV = torch.device("cuda:0")
+
+
+def _dev(a):
+    return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+@pytest.mark.parametrize("T", [1.0, 0.0])
+def test_loopback_rounds_match_oracle_in_fifo_order(T):
+    N, slots, rounds_per_stream, B, k, V = 3, 2, 4, 24, 4, 3001
+    seed = 77
+    h = star.Star(0, N + 1, B, k, V, T, seed=seed, n_slots=slots, device=DEV, transport="loopback")
+    inflight, done = {}, []
+
+    def submit(v, s, r):
+        d = make_batch(V, k, B, T, 30.0, seed=1000 * v + 10 * s + r)
+        t = {"p": _dev(d["p"]), "q": _dev(d["q"]) if T > 0 else None, "ids": _dev(d["ids"]),
+             "L": torch.full((B,), -7, dtype=torch.int32, device=DEV),
+             "tok": torch.full((B, k + 1), -7, dtype=torch.int32, device=DEV)}
+        rid = (v << 40) + (s << 20)
+        h.submit(v, s, r, t["ids"], t["q"], t["L"], t["tok"], request_id_base=rid, p=t["p"])
+        inflight[(v, s)] = (r, d, t, rid)
+
+    for s in range(slots):
+        for v in range(1, N + 1):
+            submit(v, s, 0)
+    while inflight:
+        got = h.poll(timeout_us=10_000_000)
+        assert got is not None, "no return within 10 s"
+        v, s, r = got
+        r0, d, t, rid = inflight.pop((v, s))
+        assert r == r0
+        L, tok = t["L"].cpu().numpy(), t["tok"].cpu().numpy()
+        ref = oracle.verify(d["p"], d["q"] if T > 0 else None, d["ids"], T, seed=seed, round=r,
+                            rid_base=rid, trace=True)
+        compare(d, (L, tok, np.zeros(B, np.int32)), ref, T, seed, r, rid)
+        done.append((v, s, r))
+        if r + 1 < rounds_per_stream:
+            h.draft_begin()
+            submit(v, s, r + 1)
+            h.draft_end()
+    assert sorted(done) == sorted((v, s, r) for v in range(1, N + 1) for s in range(slots)
+                                  for r in range(rounds_per_stream))
+    st = h.stats()
+    assert st["rounds"] == N * slots * rounds_per_stream
+    assert 0.0 < st["busy_fraction"] <= 1.0 + 1e-9
+    assert st["mean_wait_ms"] >= 0.0
+    h.close()
+
+
+def test_loopback_rejects_misuse():
+    h = star.Star(0, 2, 8, 2, 64, 1.0, n_slots=1, device=DEV, transport="loopback")
+    ids = torch.zeros(8, 2, dtype=torch.int32, device=DEV)
+    q = torch.zeros(8, 2, 64, device=DEV)
+    p = torch.zeros(8, 3, 64, device=DEV)
+    L = torch.empty(8, dtype=torch.int32, device=DEV)
+    tok = torch.empty(8, 3, dtype=torch.int32, device=DEV)
+    with pytest.raises(star.StarsdError, match="INVALID_ARGUMENT"):
+        h.submit(2, 0, 0, ids, q, L, tok, p=p)          # verifier out of range
+    with pytest.raises(star.StarsdError, match="INVALID_ARGUMENT"):
+        h.submit(1, 1, 0, ids, q, L, tok, p=p)          # slot out of range
+    h.submit(1, 0, 0, ids, q, L, tok, p=p)
+    with pytest.raises(star.StarsdError, match="INVALID_ARGUMENT"):
+        h.submit(1, 0, 1, ids, q, L, tok, p=p)          # slot still in flight
+    assert h.poll(timeout_us=5_000_000) == (1, 0, 0)
+    assert h.poll(timeout_us=0) is None
+    with pytest.raises(star.StarsdError, match="INVALID_ARGUMENT"):
+        h.draft_end()                                   # end without begin
+    h.close()
