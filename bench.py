@@ -92,6 +92,7 @@ class ClockSampler:
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
         self._stop = threading.Event()
+        self._first = threading.Event()
         self.max_mhz = None
         self.ok = False
         try:
@@ -115,12 +116,14 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
+            self._first.set()
             time.sleep(self.period)
 
     def __enter__(self):
         if self.ok:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            self._first.wait(timeout=2.0)      # sampling is live before the timed region
         return self
 
     def __exit__(self, *a):

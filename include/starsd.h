@@ -161,7 +161,10 @@ typedef struct {
     int32_t rank;        /* 0 = draft, 1..world-1 = verifier                                 */
     int32_t world;       /* 2..8 on one node                                                 */
     int32_t n_slots;     /* >= 2 outstanding rounds per verifier                             */
-    sd_shape max_shape;  /* upper bound of the per-round shape (B_v, k, V, dtype)            */
+    sd_shape max_shape;  /* upper bound of the per-round shape (B_v, k, V, dtype); rows are
+                            exchanged dense: ld_p = ld_q = 0 or V, and V * element size must
+                            be a multiple of 16 bytes (else SD_ERR_UNSUPPORTED /
+                            SD_ERR_INVALID_ARGUMENT)                                         */
     float temperature;   /* verify temperature (0 = greedy)                                  */
     uint64_t seed;       /* Philox key used by the verifiers                                 */
     int32_t timeout_ms;  /* per-round completion timeout before SD_ERR_TIMEOUT (0 = none)    */

@@ -23,7 +23,7 @@ def _dev(a):
 
 @pytest.mark.parametrize("T", [1.0, 0.0])
 def test_loopback_rounds_match_oracle_in_fifo_order(T):
-    N, slots, rounds_per_stream, B, k, V = 3, 2, 4, 24, 4, 3001
+    N, slots, rounds_per_stream, B, k, V = 3, 2, 4, 24, 4, 3000
     seed = 77
     h = star.Star(0, N + 1, B, k, V, T, seed=seed, n_slots=slots, device=DEV, transport="loopback")
     inflight, done = {}, []
