@@ -302,7 +302,10 @@ def run_ours(args):
     (ms_max,), (tokens_all,) = reduce_max_sum([ms], [tokens], dev)
     value = tokens_all / (ms_max / 1000.0)
 
-    # dominant kernel (k_row_stats): algorithmic bytes of the whole step per launch / its time
+    # dominant kernel (the cluster kernel, or k_row_stats on the two-launch path): algorithmic
+    # bytes of the whole step per launch / its CUDA-event time on the launching stream
+    pl = sd.plan(B, k, V, T, torch.float32 if args.dtype == "f32" else torch.bfloat16)
+    kname = {"stream": "k_verify_stream", "cluster": "k_verify_cluster"}.get(pl["variant"], "k_row_stats")
     kA_mean_ms = statistics.fmean(kA)
     alg_per_launch = alg / K
     peak, peak_kind = load_peaks()
@@ -311,7 +314,7 @@ def run_ours(args):
     prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_{args.dtype}.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("k_row_stats_dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get(f"{kname}_dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -367,7 +370,7 @@ def run_ours(args):
             "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": config_block(args, c),
-            "roofline": {"bound": "hbm", "kernel": "k_row_stats", "achieved": achieved_gbs,
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved_gbs,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg_per_launch,
@@ -375,7 +378,8 @@ def run_ours(args):
                          "step_gbs": alg_per_launch / (ms_max / K / 1000.0) / 1e9},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": K * 2,
+            "gpu_launches": K * pl["launches"],
+            "kernel_plan": pl,
             "clocks": clocks,
             "accept": {"mean_L": float(Lh.mean()), "mean_emitted": float((Lh + 1).mean()),
                        "fault_requests": int((~ok).sum())},

@@ -115,6 +115,32 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
 sd_status sd_verify_workspace_size(const sd_shape* shape, float temperature, size_t* bytes);
 
 /*
+ * sd_verify_plan -- how sd_verify will run this shape on the current device (host only; it
+ * may query the device's occupancy limits, but launches nothing).
+ *   variant      SD_VARIANT_TWO_LAUNCH (default): k_row_stats + k_sample / k_finalize_greedy;
+ *                SD_VARIANT_STREAM: one launch of `ctas` persistent CTAs in clusters of
+ *                `cluster`; each CTA streams a `slice`-logit vocabulary slice of every row pair
+ *                its cluster owns through a TMA ring (every reached logit read from HBM once);
+ *                SD_VARIANT_CLUSTER: one launch, (k+1)*B thread-block clusters of `cluster`
+ *                CTAs, each CTA holding a `slice`-logit slice of a (p_j, q_j) row pair in shared
+ *                memory (every logit read from HBM at most once);
+ *                SD_VARIANT_FUSED: one persistent cooperative launch.
+ *   launches     kernel launches per sd_verify call
+ *   cluster, slice, ctas   cluster size, logits per CTA slice, CTAs in the (first) launch
+ *   max_active_clusters, smem_bytes   occupancy of the cluster variant (0 otherwise)
+ * Environment STARSD_KERNEL=stream|cluster|fused selects another variant (default: two-launch;
+ * a variant that cannot serve a shape falls back to the two-launch path).
+ */
+enum { SD_VARIANT_CLUSTER = 0, SD_VARIANT_TWO_LAUNCH = 1, SD_VARIANT_FUSED = 2, SD_VARIANT_STREAM = 3 };
+typedef struct {
+    int32_t variant, launches, cluster, slice;
+    int64_t ctas;
+    int32_t max_active_clusters;   /* cluster variant: clusters the device keeps resident */
+    int32_t smem_bytes;            /* dynamic shared memory per CTA                        */
+} sd_plan;
+sd_status sd_verify_plan(const sd_shape* shape, float temperature, sd_plan* out);
+
+/*
  * sd_philox_uniforms -- the uniforms sd_verify draws (reading C-8), for tests and tooling.
  * For i in [0, n): counter = (pos[i], round mod 2^32, rid[i] mod 2^32, rid[i] >> 32), key = seed;
  * out_words[4 i .. 4 i + 3] = the four Philox4x32-10 output words (device, uint32).

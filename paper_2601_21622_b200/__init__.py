@@ -13,7 +13,7 @@ import torch
 from . import _lib
 from ._lib import StarsdError, check
 
-__all__ = ["verify", "verify_host", "workspace_size", "philox_words", "Workspace", "StarsdError",
+__all__ = ["verify", "verify_host", "workspace_size", "plan", "philox_words", "Workspace", "StarsdError",
            "version"]
 
 FAULT_BAD_DRAFT_ID, FAULT_NONFINITE, FAULT_EMPTY_ROW = 1, 2, 4
@@ -46,6 +46,23 @@ def workspace_size(batch: int, k: int, vocab: int, temperature: float,
     check(_lib.load().sd_verify_workspace_size(ctypes.byref(sh), float(temperature),
                                                ctypes.byref(n)), "sd_verify_workspace_size")
     return n.value
+
+
+def plan(batch: int, k: int, vocab: int, temperature: float,
+         dtype: torch.dtype = torch.float32) -> dict:
+    """How sd_verify runs this shape (sd_verify_plan): kernel variant, launches per call,
+    cluster size, logits per CTA slice, CTAs per launch."""
+    code = _lib.SD_DTYPE_F32 if dtype == torch.float32 else _lib.SD_DTYPE_BF16
+    per16 = 4 if code == _lib.SD_DTYPE_F32 else 8
+    ld = (vocab + per16 - 1) // per16 * per16
+    sh = _shape(batch, k, vocab, ld, ld, code)
+    out = _lib.Plan()
+    check(_lib.load().sd_verify_plan(ctypes.byref(sh), float(temperature), ctypes.byref(out)),
+          "sd_verify_plan")
+    return {"variant": _lib.VARIANT_NAMES.get(out.variant, str(out.variant)),
+            "launches": out.launches, "cluster": out.cluster, "slice": out.slice,
+            "ctas": out.ctas, "max_active_clusters": out.max_active_clusters,
+            "smem_bytes": out.smem_bytes}
 
 
 class Workspace:

@@ -22,12 +22,21 @@ EXPORTS = ["sd_verify", "sd_verify_workspace_size", "sd_philox_uniforms", "sd_st
            "sd_star_create", "sd_star_round", "sd_star_poll", "sd_star_draft_begin",
            "sd_star_draft_end", "sd_star_stats", "sd_star_destroy", "sd_status_string",
            "sd_last_error", "sd_version", "sd_profile_events", "sd_debug_trace",
-           "sd_star_simulate"]
+           "sd_star_simulate", "sd_verify_plan"]
 
 
 class Shape(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("k", ctypes.c_int32), ("vocab", ctypes.c_int32),
                 ("ld_p", ctypes.c_int64), ("ld_q", ctypes.c_int64), ("dtype", ctypes.c_int32)]
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [("variant", ctypes.c_int32), ("launches", ctypes.c_int32),
+                ("cluster", ctypes.c_int32), ("slice", ctypes.c_int32), ("ctas", ctypes.c_int64),
+                ("max_active_clusters", ctypes.c_int32), ("smem_bytes", ctypes.c_int32)]
+
+
+VARIANT_NAMES = {0: "cluster", 1: "two_launch", 2: "fused", 3: "stream"}
 
 
 class StarConfig(ctypes.Structure):
@@ -79,6 +88,8 @@ def load():
     L.sd_verify_workspace_size.argtypes = [ctypes.POINTER(Shape), ctypes.c_float,
                                            ctypes.POINTER(sz)]
     L.sd_verify_workspace_size.restype = st
+    L.sd_verify_plan.argtypes = [ctypes.POINTER(Shape), ctypes.c_float, ctypes.POINTER(Plan)]
+    L.sd_verify_plan.restype = st
     L.sd_philox_uniforms.argtypes = [u64, u64, vp, vp, i32, vp, vp]
     L.sd_philox_uniforms.restype = st
     L.sd_star_unique_ids.argtypes = [i32, vp]

@@ -47,6 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-I", os.path.join(ROOT, "include")]
     if verbose:
         cmd += ["-Xptxas", "-v"]
+    if os.environ.get("STARSD_BUILD_DEBUG"):
+        cmd += ["-DSD_STREAM_DEBUG=1"]
     if inc:
         cmd += ["-DSD_WITH_NCCL=1", "-I", inc]
     tmp = LIB + f".tmp{os.getpid()}"

@@ -35,17 +35,32 @@ sd_status fail(sd_status s, const char* fmt, ...) {
 void clear_error() { g_err[0] = '\0'; }
 const char* last_error() { return g_err; }
 
-// Default: the two-launch path (k_row_stats + k_sample, PDL-chained), measured faster on B200
-// for every BASELINE config.  STARSD_KERNEL=fused selects the single persistent warp-
-// specialized kernel (verify_fused.cu) -- kept as a cross-variant parity check and for study.
-static bool use_v1() {
+// Kernel variant.  Default: the two-launch path (verify_kernels.cu: k_row_stats + k_sample /
+// k_finalize_greedy, PDL-chained), measured fastest on B200 for every BASELINE config this round.
+// STARSD_KERNEL=stream / cluster / fused select the persistent warp-specialized cluster kernel
+// (verify_stream.cu), the row-holding cluster kernel (verify_cluster.cu) or the persistent
+// cooperative kernel (verify_fused.cu): cross-variant parity checks and study.
+enum Variant { kCluster = 0, kTwoLaunch = 1, kFused = 2, kStream = 3 };
+static Variant variant() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("STARSD_KERNEL");
-        v = (e && strcmp(e, "fused") == 0) ? 0 : 1;
+        v = kTwoLaunch;
+        if (e && strcmp(e, "stream") == 0) v = kStream;
+        if (e && strcmp(e, "cluster") == 0) v = kCluster;
+        if (e && strcmp(e, "fused") == 0) v = kFused;
     }
-    return v == 1;
+    return static_cast<Variant>(v);
 }
+
+bool stream_config(int32_t V, int esz, bool greedy, StreamPlan* out);
+cudaError_t launch_stream(const SParams& P, bool greedy, bool bf16, size_t smem, cudaStream_t st,
+                          cudaEvent_t ev0, cudaEvent_t ev1);
+bool cluster_config(int32_t V, int esz, bool greedy, int32_t* C, int32_t* W, int32_t* nvr,
+                    size_t* smem);
+int cluster_max_active(int32_t V, int esz, bool greedy);
+cudaError_t launch_cluster(const CParams& P, bool greedy, bool bf16, size_t smem, cudaStream_t st,
+                           cudaEvent_t ev0, cudaEvent_t ev1);
 
 void record_event(cudaEvent_t ev, cudaStream_t st);
 
@@ -138,7 +153,7 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     // c2 = log2(e) / T rounded to fp32; every exponent in the kernels uses this one constant
     const float c2 =
         greedy ? 0.0f : static_cast<float>(1.4426950408889634 / static_cast<double>(temperature));
-    if (!use_v1()) {
+    if (variant() == kFused) {
         const int32_t esz_ = esz;
         for (int32_t off = 0; off < shape->batch; off += kFusedMaxBatch) {
             const int32_t Bl = shape->batch - off < kFusedMaxBatch ? shape->batch - off : kFusedMaxBatch;
@@ -198,6 +213,75 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
         return SD_OK;
     }
     const WsLayout w = ws_layout(shape->batch, shape->k, shape->vocab, esz);
+    char* ws = static_cast<char*>(workspace);
+    StreamPlan sp;
+    if (variant() == kStream && stream_config(shape->vocab, esz, greedy, &sp)) {
+        SParams S{};
+        S.p = p_logits;
+        S.q = greedy ? nullptr : q_logits;
+        S.ids = draft_ids;
+        S.B = shape->batch;
+        S.k = shape->k;
+        S.V = shape->vocab;
+        S.ld_p = shape->ld_p ? shape->ld_p : shape->vocab;
+        S.ld_q = shape->ld_q ? shape->ld_q : shape->vocab;
+        S.C = sp.C;
+        S.G = sp.G;
+        S.W = sp.W;
+        S.segmax = sp.segmax;
+        S.nslot = sp.nslot;
+        S.c2 = c2;
+        S.seed = seed;
+        S.round = round;
+        S.rid_base = request_id_base;
+        S.out_L = out_accept_len;
+        S.out_tok = out_tokens;
+        S.out_status = out_status;
+        S.rej_mask = reinterpret_cast<uint32_t*>(ws + w.rej_mask);
+        S.ticket = reinterpret_cast<uint32_t*>(ws + w.ticketB);
+        S.rowres = reinterpret_cast<int2*>(ws + w.rowstat);
+        S.trace = g_trace;
+        {
+            static int dbg = -1;
+            if (dbg < 0) {
+                const char* e = getenv("STARSD_DEBUG");
+                dbg = e ? atoi(e) : 0;
+            }
+            S.debug = dbg;
+        }
+        cudaError_t e = launch_stream(S, greedy, shape->dtype == SD_DTYPE_BF16, sp.smem, stream, ev0, ev1);
+        if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+        return SD_OK;
+    }
+    int32_t cC, cW, cnvr;
+    size_t csmem;
+    if (variant() == kCluster && cluster_config(shape->vocab, esz, greedy, &cC, &cW, &cnvr, &csmem)) {
+        CParams C{};
+        C.p = p_logits;
+        C.q = greedy ? nullptr : q_logits;
+        C.ids = draft_ids;
+        C.B = shape->batch;
+        C.k = shape->k;
+        C.V = shape->vocab;
+        C.ld_p = shape->ld_p ? shape->ld_p : shape->vocab;
+        C.ld_q = shape->ld_q ? shape->ld_q : shape->vocab;
+        C.C = cC;
+        C.W = cW;
+        C.nvr = cnvr;
+        C.c2 = c2;
+        C.seed = seed;
+        C.round = round;
+        C.rid_base = request_id_base;
+        C.out_L = out_accept_len;
+        C.out_tok = out_tokens;
+        C.out_status = out_status;
+        C.rej_mask = reinterpret_cast<uint32_t*>(ws + w.rej_mask);
+        C.ticket = reinterpret_cast<uint32_t*>(ws + w.ticketB);
+        C.rowres = reinterpret_cast<int2*>(ws + w.rowstat);
+        cudaError_t e = launch_cluster(C, greedy, shape->dtype == SD_DTYPE_BF16, csmem, stream, ev0, ev1);
+        if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+        return SD_OK;
+    }
 
     Params P{};
     P.p = p_logits;
@@ -218,7 +302,6 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     P.out_L = out_accept_len;
     P.out_tok = out_tokens;
     P.out_status = out_status;
-    char* ws = static_cast<char*>(workspace);
     P.rej_mask = reinterpret_cast<uint32_t*>(ws + w.rej_mask);
     P.ticketA = reinterpret_cast<uint32_t*>(ws + w.ticketA);
     P.ticketB = reinterpret_cast<uint32_t*>(ws + w.ticketB);
@@ -229,6 +312,51 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
 
     cudaError_t e = launch_verify(P, greedy, shape->dtype == SD_DTYPE_BF16, stream, ev0, ev1);
     if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return SD_OK;
+}
+
+sd_status sd_verify_plan(const sd_shape* shape, float temperature, sd_plan* out) {
+    clear_error();
+    int esz;
+    sd_status s = check_shape(shape, temperature, &esz);
+    if (s != SD_OK) return s;
+    if (!out) return fail(SD_ERR_INVALID_ARGUMENT, "out is NULL");
+    const bool greedy = temperature == 0.0f;
+    int32_t cC, cW, cnvr;
+    size_t csmem;
+    *out = sd_plan{};
+    StreamPlan sp;
+    if (variant() == kStream && stream_config(shape->vocab, esz, greedy, &sp)) {
+        out->variant = SD_VARIANT_STREAM;
+        out->launches = 1;
+        out->cluster = sp.C;
+        out->slice = sp.W;
+        out->ctas = (int64_t)sp.G * sp.C;
+        out->max_active_clusters = sp.G;
+        out->smem_bytes = (int32_t)sp.smem;
+        return SD_OK;
+    }
+    if (variant() == kCluster && cluster_config(shape->vocab, esz, greedy, &cC, &cW, &cnvr, &csmem)) {
+        out->variant = SD_VARIANT_CLUSTER;
+        out->launches = 1;
+        out->cluster = cC;
+        out->slice = cW;
+        out->ctas = (int64_t)(shape->k + 1) * shape->batch * cC;
+        out->max_active_clusters = cluster_max_active(shape->vocab, esz, greedy);
+        out->smem_bytes = (int32_t)csmem;
+        return SD_OK;
+    }
+    if (variant() == kFused) {
+        out->variant = SD_VARIANT_FUSED;
+        out->launches = (shape->batch + kFusedMaxBatch - 1) / kFusedMaxBatch;
+        return SD_OK;
+    }
+    int32_t nch, CH;
+    chunking(shape->vocab, esz, &nch, &CH);
+    out->variant = SD_VARIANT_TWO_LAUNCH;
+    out->launches = 2;
+    out->slice = CH;
+    out->ctas = (int64_t)(shape->k + 1) * shape->batch * nch;
     return SD_OK;
 }
 

@@ -10,13 +10,13 @@ constexpr int kThreads = 256;            // threads per CTA (8 warps)
 constexpr int kWarps = kThreads / 32;
 constexpr int kVecBytes = 16;            // one 128-bit smem/global vector per thread per tile
 constexpr int kTileBytes = kThreads * kVecBytes;   // 4 KB of one row per tile
-constexpr int kMaxChunkBytes = 16 * 1024;          // one CTA owns <= 16 KB of a row
-                                                   // (16 KB bulk copies stream at ~7.3 TB/s)
+constexpr int kMaxChunkBytes = 32 * 1024;          // one CTA owns <= 32 KB of a row
+                                                   // (one 32 KB bulk copy per row and CTA)
 
 // Per (request b, position j, vocab chunk c): what one kernel-A CTA found in its slice.
 struct PartA {
-    double S_p, S_q;     // sum over the slice of 2^((z - M_c) * c2), c2 = log2(e)/T (fp64 accum)
-    float M_p, M_q;      // slice max of the raw logits
+    double S_p, S_q;     // sum over the slice of 2^(z c2 - D_c), c2 = log2(e)/T (fp64 across threads)
+    float M_p, M_q;      // sampled: slice's scaled max D_c = max fl(z_max c2); greedy: raw max
     float zx_p, zx_q;    // z_p,j(x_j), z_q,j(x_j) if x_j lies in this slice
     int32_t flags;       // kPartNonfiniteP | kPartNonfiniteQ | kPartHasX
     int32_t argmax;      // greedy: lowest index of the slice max (global token id)
@@ -26,8 +26,8 @@ constexpr int32_t kPartNonfiniteP = 1, kPartNonfiniteQ = 2, kPartHasX = 4;
 // Per (request b, position j): the whole-row statistics, written by the last kernel-A CTA of
 // that row pair, read by the sampling kernel.
 struct RowStat {
-    double S_p, S_q;     // row sums relative to the row max (same scale as PartA)
-    float M_p, M_q;      // row max
+    double S_p, S_q;     // row sums of 2^(z c2 - D) (same scale as PartA)
+    float M_p, M_q;      // sampled: scaled row maxima D = max fl(z_max c2); greedy: raw max of p
     int32_t status;      // SD_FAULT_* bits decided at this position
     int32_t argmax;      // greedy: argmax of p row (lowest index)
 };
@@ -85,7 +85,7 @@ inline void chunking(int32_t V, int32_t esz, int32_t* nch, int32_t* CH) {
 inline WsLayout ws_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
     int32_t nch, CH;
     chunking(V, esz, &nch, &CH);
-    const int64_t nseg = CH / (32 * (kVecBytes / esz));
+    const int64_t nseg = CH / (32 * (kVecBytes / esz));   // 32-vector segments per chunk
     WsLayout w{};
     size_t o = 0;
     w.rej_mask = o; o = align16(o + sizeof(uint32_t) * B);
@@ -99,6 +99,72 @@ inline WsLayout ws_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
     w.total = o;
     return w;
 }
+
+// ---- cluster (v3) kernel: one thread-block cluster per (request, position) row pair --------
+constexpr int kCThreads = 256;      // threads per CTA
+constexpr int kCMaxPieces = 14;     // 16 KB bulk copies per row slice (<= 224 KB)
+
+struct CParams {
+    const void* p;
+    const void* q;
+    const int32_t* ids;
+    int32_t B, k, V;
+    int64_t ld_p, ld_q;          // elements
+    int32_t C;                   // CTAs per cluster (1..16)
+    int32_t W;                   // vocabulary slice per CTA (elements, multiple of 16 bytes)
+    int32_t nvr;                 // 16-byte vectors per thread in the residual pass (odd)
+    float c2;                    // log2(e) / T in fp32 (0 for greedy)
+    uint64_t seed, round, rid_base;
+    int32_t* out_L;
+    int32_t* out_tok;
+    int32_t* out_status;
+    uint32_t* rej_mask;          // [B] bit j: position j stopped the chain (zero region)
+    uint32_t* ticket;            // [B] rows of the request finished (zero region)
+    int2* rowres;                // [B][k+1] (token, status) of a stopping / bonus row
+};
+
+// ---- stream (v4) kernel: persistent warp-specialized clusters --------------------------------
+constexpr int kSStatsWarps = 8;
+constexpr int kSRowWarps = 4;
+constexpr int kSProducers = 2;             // producer lanes issuing main-ring copies (tools/tma_probe:
+                                           // 2 threads x 32 KB copies saturate HBM)
+constexpr int kSThreads = 32 * (1 + kSStatsWarps + kSRowWarps + 1);   // + main / residual producers
+constexpr uint32_t kSPieceBytes = 32768;   // ring slot = one 32 KB bulk copy (tools/tma_probe:
+                                           // one issuing thread sustains ~49 GB/s/SM with 32 KB
+                                           // copies, ~25 GB/s/SM with 16 KB)
+constexpr int kSMaxSlots = 16;
+constexpr int kSResSlots = 2;              // residual re-read ring (one p/q piece pair)
+
+struct SParams {
+    const void* p;
+    const void* q;
+    const int32_t* ids;
+    int32_t B, k, V;
+    int64_t ld_p, ld_q;          // elements
+    int32_t C, G;                // CTAs per cluster, persistent clusters
+    int32_t W;                   // vocabulary slice per CTA (elements, multiple of 16 bytes)
+    int32_t segmax;              // residual segments per slice (table stride)
+    int32_t nslot;               // ring slots
+    float c2;                    // log2(e) / T in fp32 (0 for greedy)
+    uint64_t seed, round, rid_base;
+    int32_t* out_L;
+    int32_t* out_tok;
+    int32_t* out_status;
+    uint32_t* rej_mask;          // [B] bit j: position j stopped the chain (zero region)
+    uint32_t* ticket;            // [B] rows of the request finished (zero region)
+    int2* rowres;                // [B][k+1] (token, status) of a stopping / bonus row
+    unsigned long long* trace;   // development event log (nullptr in production), see below
+    int32_t debug;               // development knobs (0 in production): bit0 stats warps skip the
+                                 // arithmetic (bandwidth probe; results are wrong)
+};
+// trace layout: [grid][kSTraceN] records ((type << 56) | (arg << 40) | (globaltimer & 2^40-1));
+// record 0 of a CTA holds the number of records it wrote.
+constexpr int kSTraceN = 8192;
+
+struct StreamPlan {
+    int32_t C, G, W, segmax, nslot;
+    size_t smem;
+};
 
 // ---- fused (v2) kernel: parameters and workspace layout ----------------------------------
 namespace fused {

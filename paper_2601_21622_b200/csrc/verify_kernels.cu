@@ -36,6 +36,7 @@ namespace sd {
 // status bits (values of include/starsd.h SD_FAULT_*)
 constexpr int32_t kBadId = 1, kNonfinite = 2, kEmptyRow = 4, kZeroQ = 8, kZeroResidual = 16;
 constexpr int32_t kHard = kBadId | kNonfinite | kEmptyRow;
+constexpr int kGridY = 32768;   // requests per grid.y span (gridDim.y <= 65535)
 constexpr uint32_t kSkipArrive = 1u | (1u << 16);
 
 // ------------------------------------------------------------------------------------------
@@ -131,9 +132,86 @@ __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
 
 // Probability terms of the sampling pass.  Written with explicit-rounding intrinsics so the
 // main pass and the final re-read compute bit-identical values.
-//   p(x) = 2^((z_p - M_p) c2) / S_p ,  r(x) = max(0, p(x) - q(x))   (fp64 after the exp)
-__device__ __forceinline__ double prob_term(float z, float M, float c2, double invS) {
-    return __dmul_rn(static_cast<double>(ex2_approx(__fmul_rn(__fsub_rn(z, M), c2))), invS);
+//   p(x) = 2^(z_p c2 - D_p) / S_p ,  r(x) = max(0, p(x) - q(x))   (fp64 after the exp)
+// D is the row's scaled maximum (the largest fl(z_max c2) of the stats pass), S the sum of
+// 2^(z c2 - D) over the row.
+__device__ __forceinline__ double prob_term(float z, float D, float c2, double invS) {
+    return __dmul_rn(static_cast<double>(ex2_approx(__fmaf_rn(z, c2, -D))), invS);
+}
+
+// ---- lean arithmetic of the stats pass (FMNMX3, FFMA2, MUFU.EX2, FADD2) ----------------------
+__device__ __forceinline__ float max3nan(float a, float b, float c) {
+    float d;
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long pk2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void upk2(unsigned long long r, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long ex2x2(unsigned long long a) {
+    float lo, hi;
+    upk2(a, lo, hi);
+    return pk2(ex2_approx(lo), ex2_approx(hi));
+}
+
+// One thread's (d, s) over its NV x VEC register-resident logits (-inf padded): d = fl(max * c2),
+// s = sum of 2^(z c2 - d).  A NaN or +inf sets the fault flag (the max propagates it).
+template <int NV, int VEC>
+__device__ __forceinline__ void thread_stats(const float (&v)[NV][VEC], float c2, int flag, float& d,
+                                             float& s, int& nf) {
+    float mv[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        float t = max3nan(v[i][0], v[i][1], v[i][2]);
+#pragma unroll
+        for (int e = 3; e < VEC; e += 2) t = max3nan(t, v[i][e], v[i][e + 1 < VEC ? e + 1 : e]);
+        mv[i] = t;
+    }
+    float m = mv[0];
+#pragma unroll
+    for (int i = 1; i < NV; i += 2) m = max3nan(m, mv[i], mv[i + 1 < NV ? i + 1 : i]);
+    d = -INFINITY;
+    s = 0.0f;
+    if (!(m < INFINITY)) {
+        nf |= flag;                 // NaN or +inf
+        return;
+    }
+    if (!(m > -INFINITY)) return;   // nothing finite here
+    d = m * c2;
+    const unsigned long long cc = pk2(c2, c2), nd = pk2(-d, -d);
+    unsigned long long a[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int e = 0; e < VEC; e += 2) {
+            const int k = (i * (VEC / 2) + e / 2) & 3;
+            a[k] = fadd2(a[k], ex2x2(ffma2(pk2(v[i][e], v[i][e + 1]), cc, nd)));
+        }
+    const unsigned long long t = fadd2(fadd2(a[0], a[1]), fadd2(a[2], a[3]));
+    float x0, x1;
+    upk2(t, x0, x1);
+    s = x0 + x1;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -142,24 +220,35 @@ template <typename E, bool GREEDY>
 __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
     using EL = Elt<E>;
     constexpr int VEC = EL::VEC;
-    constexpr int TILE = kThreads * VEC;
+    constexpr int NV = kMaxChunkBytes / kVecBytes / kThreads;   // 16-byte vectors per thread
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t bar[2];
     __shared__ int s_flag;
-    __shared__ float s_mp[kWarps], s_mq[kWarps];
-    __shared__ int s_gi[kWarps];
-    __shared__ double s_sp[kWarps], s_sq[kWarps];
+    __shared__ float s_d[2][kWarps];
+    __shared__ double s_s[2][kWarps];
+    __shared__ int s_gi[kWarps], s_f[kWarps];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nch = P.nch, kk = P.k;
-    const int c = blockIdx.x % nch;
-    const int rowid = blockIdx.x / nch;          // = j * B + b  (position-major)
-    const int b = rowid % P.B, j = rowid / P.B;
+    // grid (chunk, request, position): blocks are scheduled x-fastest, so all requests'
+    // position 0 come first (position-major), without any integer division
+    // grid.y covers at most kGridY requests; grid.z = (k+1) * ceil(B / kGridY) (position-major)
+    const int c = blockIdx.x;
+    int b = blockIdx.y, j = blockIdx.z;
+    if (P.B > kGridY) {
+        const int nb = (P.B + kGridY - 1) / kGridY;
+        b += (j % nb) * kGridY;
+        j /= nb;
+        if (b >= P.B) return;
+    }
     const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
 
     if (tid == 0) {
-        const uint32_t m = ld_relaxed_u32(P.rej_mask + b);
+        const uint32_t m = j ? ld_relaxed_u32(P.rej_mask + b) : 0u;
         s_flag = (m & ((1u << j) - 1u)) != 0u;
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
     }
     __syncthreads();
     if (s_flag) {   // the request already stopped before j: this row is never needed
@@ -181,18 +270,14 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
     E* sq = sp + P.CH;
     const uint32_t bytes = static_cast<uint32_t>(len) * sizeof(E);
     const uint32_t bulk = bytes & ~15u;
-
+    // p and q slices are copied by threads of different warps: bulk copies issued by one thread
+    // complete one after another (tools/tma_probe)
     if (tid == 0) {
-        mbar_init(&bar, 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (tid == 0) {
-        mbar_arrive_expect_tx(&bar, load_q ? 2u * bulk : bulk);
-        if (bulk) {
-            bulk_g2s(sp, gp, bulk, &bar);
-            if (load_q) bulk_g2s(sq, gq, bulk, &bar);
-        }
+        mbar_arrive_expect_tx(&bar[0], bulk);
+        if (bulk) bulk_g2s(sp, gp, bulk, &bar[0]);
+    } else if (tid == 32 && load_q) {
+        mbar_arrive_expect_tx(&bar[1], bulk);
+        if (bulk) bulk_g2s(sq, gq, bulk, &bar[1]);
     }
     for (int i = static_cast<int>(bulk / sizeof(E)) + tid; i < len; i += kThreads) {
         sp[i] = gp[i];
@@ -200,187 +285,137 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
     }
     const int x = (j < kk) ? P.ids[static_cast<size_t>(b) * kk + j] : -1;
     __syncthreads();
-    mbar_wait(&bar, 0);
 
-    // ---- sweep 1: slice max (NaN-propagating: a NaN makes the max NaN, +inf makes it +inf,
-    // so faults need no per-element test); greedy: lowest argmax + NaN-propagating max ------
-    const int nvec = len / VEC;                  // fully valid vectors
-    const bool tail = nvec * VEC < len;          // a ragged last vector (row end only)
-    const int tail_tid = nvec % kThreads;
-    float mp = -INFINITY, mq = -INFINITY, np = -INFINITY;
-    int gi = INT_MAX;
-#pragma unroll 4
-    for (int g = tid; g < nvec; g += kThreads) {
-        float v[VEC];
-        EL::unpack(*reinterpret_cast<const uint4*>(sp + g * VEC), v);
-        if (GREEDY) {
+    // ---- registers: NV vectors of p (and q) per thread; -inf past the slice end ------------
+    const int nfull = len / VEC;                 // complete vectors
+    const int nvv = (len + VEC - 1) / VEC;       // vectors incl. a ragged last one
+    float vp[NV][VEC];
+    mbar_wait(&bar[0], 0);
 #pragma unroll
-            for (int u = 0; u < VEC; ++u) {
-                np = fmax_nan(np, v[u]);
-                if (v[u] > mp) {
-                    mp = v[u];
-                    gi = c0 + g * VEC + u;
-                }
-            }
+    for (int i = 0; i < NV; ++i) {
+        const int g = tid + i * kThreads;
+        if (g < nfull) {
+            EL::unpack(*reinterpret_cast<const uint4*>(sp + g * VEC), vp[i]);
         } else {
 #pragma unroll
-            for (int u = 0; u < VEC; u += 2) mp = fmax_nan(mp, fmax_nan(v[u], v[u + 1]));
-            if (load_q) {
-                EL::unpack(*reinterpret_cast<const uint4*>(sq + g * VEC), v);
+            for (int e = 0; e < VEC; ++e) vp[i][e] = -INFINITY;
+            if (g < nvv) {   // ragged last vector (row end only)
 #pragma unroll
-                for (int u = 0; u < VEC; u += 2) mq = fmax_nan(mq, fmax_nan(v[u], v[u + 1]));
+                for (int e = 0; e < VEC; ++e)
+                    if (g * VEC + e < len) vp[i][e] = EL::one(sp, g * VEC + e);
             }
         }
     }
-    if (tail && tid == tail_tid) {
-        float v[VEC];
-        EL::unpack(*reinterpret_cast<const uint4*>(sp + nvec * VEC), v);
-        for (int u = 0; u < VEC; ++u) {
-            if (nvec * VEC + u < len) {
-                if (GREEDY) {
-                    np = fmax_nan(np, v[u]);
-                    if (v[u] > mp) {
-                        mp = v[u];
-                        gi = c0 + nvec * VEC + u;
-                    }
+    int nf = 0;
+    float dP = -INFINITY, dQ = -INFINITY, sP = 0.0f, sQ = 0.0f;
+    float gbest = -INFINITY;
+    int gidx = INT_MAX;
+    if (GREEDY) {
+        float nanacc = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            float vm = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < VEC; e += 2) {
+                nanacc = max3nan(nanacc, vp[i][e], vp[i][e + 1]);
+                vm = max3(vm, vp[i][e], vp[i][e + 1]);
+            }
+            if (vm > gbest) {   // ascending index within the thread: strict > keeps the first
+                int fe = 0;
+#pragma unroll
+                for (int e = VEC - 1; e >= 0; --e)
+                    if (vp[i][e] == vm) fe = e;
+                gbest = vm;
+                gidx = c0 + (tid + i * kThreads) * VEC + fe;
+            }
+        }
+        if (!(nanacc < INFINITY)) nf |= kPartNonfiniteP;
+    } else {
+        thread_stats<NV, VEC>(vp, P.c2, kPartNonfiniteP, dP, sP, nf);
+        if (load_q) {
+            float vq[NV][VEC];
+            mbar_wait(&bar[1], 0);
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int g = tid + i * kThreads;
+                if (g < nfull) {
+                    EL::unpack(*reinterpret_cast<const uint4*>(sq + g * VEC), vq[i]);
                 } else {
-                    mp = fmax_nan(mp, v[u]);
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) vq[i][e] = -INFINITY;
+                    if (g < nvv) {
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e)
+                            if (g * VEC + e < len) vq[i][e] = EL::one(sq, g * VEC + e);
+                    }
                 }
             }
-        }
-        if (load_q) {
-            EL::unpack(*reinterpret_cast<const uint4*>(sq + nvec * VEC), v);
-            for (int u = 0; u < VEC; ++u)
-                if (nvec * VEC + u < len) mq = fmax_nan(mq, v[u]);
+            thread_stats<NV, VEC>(vq, P.c2, kPartNonfiniteQ, dQ, sQ, nf);
         }
     }
+
+    // ---- block reduction: warps, then warp 0 ---------------------------------------------
+    nf = __reduce_or_sync(0xFFFFFFFFu, nf);
     if (GREEDY) {
-        warp_argmax(mp, gi);
-        np = warp_max_nan(np);
+        float v = gbest;
+        int i = gidx;
+        warp_argmax(v, i);
+        if (lane == 0) {
+            s_d[0][warp] = v;
+            s_gi[warp] = i;
+            s_f[warp] = nf;
+        }
     } else {
-        mp = warp_max_nan(mp);
-        mq = warp_max_nan(mq);
-    }
-    if (lane == 0) {
-        s_mp[warp] = mp;
-        s_mq[warp] = GREEDY ? np : mq;
-        s_gi[warp] = gi;
+        const float Dw = warp_max(dP), Ew = warp_max(dQ);
+        const double Sw = warp_sum(sP > 0.0f ? static_cast<double>(sP * ex2_approx(dP - Dw)) : 0.0);
+        const double Tw = warp_sum(sQ > 0.0f ? static_cast<double>(sQ * ex2_approx(dQ - Ew)) : 0.0);
+        if (lane == 0) {
+            s_d[0][warp] = Dw;
+            s_d[1][warp] = Ew;
+            s_s[0][warp] = Sw;
+            s_s[1][warp] = Tw;
+            s_f[warp] = nf;
+        }
     }
     __syncthreads();
-    float Mp = s_mp[0], Mq = s_mq[0];
-    int G = s_gi[0];
-#pragma unroll
-    for (int w = 1; w < kWarps; ++w) {
-        if (GREEDY) {
-            if (s_mp[w] > Mp || (s_mp[w] == Mp && s_gi[w] < G)) {
-                Mp = s_mp[w];
-                G = s_gi[w];
-            }
-            Mq = fmax_nan(Mq, s_mq[w]);       // greedy: NaN-propagating max of p
-        } else {
-            Mp = fmax_nan(Mp, s_mp[w]);
-            Mq = fmax_nan(Mq, s_mq[w]);
-        }
-    }
-    int bad = 0;
-    if (GREEDY) {
-        bad = (Mq != Mq || Mq == INFINITY) ? kPartNonfiniteP : 0;
-        Mq = -INFINITY;
-    } else {
-        bad = ((Mp != Mp || Mp == INFINITY) ? kPartNonfiniteP : 0) |
-              ((Mq != Mq || Mq == INFINITY) ? kPartNonfiniteQ : 0);
-    }
-
-    // ---- sweep 2: sum of 2^((z - M) c2) against the CTA max (one MUFU.EX2 per element;
-    // fp32 within a vector, fp64 across vectors) ----------------------------------------------
-    double Sp = 0.0, Sq = 0.0;
-    if (!GREEDY) {
-        const float c2 = P.c2;
-        const bool okp = Mp > -INFINITY && Mp < INFINITY;
-        const bool okq = load_q && Mq > -INFINITY && Mq < INFINITY;
-        const float ep = okp ? Mp : 0.0f, eq = okq ? Mq : 0.0f;
-        if (okp || okq) {
-#pragma unroll 4
-            for (int g = tid; g < nvec; g += kThreads) {
-                float v[VEC];
-                if (okp) {
-                    EL::unpack(*reinterpret_cast<const uint4*>(sp + g * VEC), v);
-                    float a0 = 0.0f, a1 = 0.0f;
-#pragma unroll
-                    for (int u = 0; u < VEC; u += 2) {
-                        a0 += ex2_approx(__fmul_rn(__fsub_rn(v[u], ep), c2));
-                        a1 += ex2_approx(__fmul_rn(__fsub_rn(v[u + 1], ep), c2));
-                    }
-                    Sp += static_cast<double>(a0 + a1);
-                }
-                if (okq) {
-                    EL::unpack(*reinterpret_cast<const uint4*>(sq + g * VEC), v);
-                    float a0 = 0.0f, a1 = 0.0f;
-#pragma unroll
-                    for (int u = 0; u < VEC; u += 2) {
-                        a0 += ex2_approx(__fmul_rn(__fsub_rn(v[u], eq), c2));
-                        a1 += ex2_approx(__fmul_rn(__fsub_rn(v[u + 1], eq), c2));
-                    }
-                    Sq += static_cast<double>(a0 + a1);
-                }
-            }
-            if (tail && tid == tail_tid) {
-                float v[VEC];
-                if (okp) {
-                    EL::unpack(*reinterpret_cast<const uint4*>(sp + nvec * VEC), v);
-                    float t = 0.0f;
-                    for (int u = 0; u < VEC; ++u)
-                        if (nvec * VEC + u < len) t += ex2_approx(__fmul_rn(__fsub_rn(v[u], ep), c2));
-                    Sp += static_cast<double>(t);
-                }
-                if (okq) {
-                    EL::unpack(*reinterpret_cast<const uint4*>(sq + nvec * VEC), v);
-                    float t = 0.0f;
-                    for (int u = 0; u < VEC; ++u)
-                        if (nvec * VEC + u < len) t += ex2_approx(__fmul_rn(__fsub_rn(v[u], eq), c2));
-                    Sq += static_cast<double>(t);
-                }
-            }
-        }
-        Sp = warp_sum(Sp);
-        Sq = warp_sum(Sq);
-        if (lane == 0) {
-            s_sp[warp] = Sp;
-            s_sq[warp] = Sq;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            Sp = 0.0;
-            Sq = 0.0;
-            for (int w = 0; w < kWarps; ++w) {
-                Sp += s_sp[w];
-                Sq += s_sq[w];
-            }
-        }
-    }
-
-    // ---- publish the slice, take a ticket ------------------------------------------------
-    if (tid == 0) {
+    if (warp == 0) {
+        const bool on = lane < kWarps;
+        const int f = __reduce_or_sync(0xFFFFFFFFu, on ? s_f[lane] : 0);
         PartA pa;
-        pa.S_p = Sp;
-        pa.S_q = Sq;
-        pa.M_p = Mp;
-        pa.M_q = Mq;
-        pa.zx_p = 0.0f;
-        pa.zx_q = 0.0f;
-        pa.flags = bad;
-        pa.argmax = G;
-        if (x >= c0 && x < c0 + len) {
-            pa.zx_p = EL::one(sp, x - c0);
-            pa.zx_q = load_q ? EL::one(sq, x - c0) : 0.0f;
-            pa.flags |= kPartHasX;
+        if (GREEDY) {
+            float v = on ? s_d[0][lane] : -INFINITY;
+            int i = on ? s_gi[lane] : INT_MAX;
+            warp_argmax(v, i);
+            pa.M_p = v;
+            pa.M_q = -INFINITY;
+            pa.S_p = pa.S_q = 0.0;
+            pa.argmax = i;
+        } else {
+            const float wd = on ? s_d[0][lane] : -INFINITY, we = on ? s_d[1][lane] : -INFINITY;
+            const double ws = on ? s_s[0][lane] : 0.0, wt = on ? s_s[1][lane] : 0.0;
+            const float Dc = warp_max(wd), Ec = warp_max(we);
+            pa.S_p = warp_sum(ws > 0.0 ? ws * static_cast<double>(ex2_approx(wd - Dc)) : 0.0);
+            pa.S_q = warp_sum(wt > 0.0 ? wt * static_cast<double>(ex2_approx(we - Ec)) : 0.0);
+            pa.M_p = Dc;   // scaled maxima D (see prob_term)
+            pa.M_q = Ec;
+            pa.argmax = INT_MAX;
         }
-        P.partA[pos * nch + c] = pa;
-        __threadfence();
-        const uint32_t t = atomicAdd(P.ticketA + pos, 1u);
-        const bool last = (t & 0xFFFFu) == static_cast<uint32_t>(nch - 1);
-        if (last) P.ticketA[pos] = 0u;
-        s_flag = last && (t >> 16) == 0u;   // last arriver and no slice of this row skipped
+        if (lane == 0) {
+            pa.zx_p = 0.0f;
+            pa.zx_q = 0.0f;
+            pa.flags = f;
+            if (x >= c0 && x < c0 + len) {
+                pa.zx_p = EL::one(sp, x - c0);
+                pa.zx_q = load_q ? EL::one(sq, x - c0) : 0.0f;
+                pa.flags |= kPartHasX;
+            }
+            P.partA[pos * nch + c] = pa;
+            __threadfence();
+            const uint32_t t = atomicAdd(P.ticketA + pos, 1u);
+            const bool last = (t & 0xFFFFu) == static_cast<uint32_t>(nch - 1);
+            if (last) P.ticketA[pos] = 0u;
+            s_flag = last && (t >> 16) == 0u;   // last arriver and no slice of this row skipped
+        }
     }
     __syncthreads();
     if (!s_flag || warp != 0) return;
@@ -404,15 +439,15 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
                 RG = a.argmax;
             }
         } else {
-            RMp = fmax_nan(RMp, a.M_p);
-            RMq = fmax_nan(RMq, a.M_q);
+            RMp = fmaxf(RMp, a.M_p);
+            RMq = fmaxf(RMq, a.M_q);
         }
     }
     if (GREEDY) {
         warp_argmax(RMp, RG);
     } else {
-        RMp = warp_max_nan(RMp);
-        RMq = warp_max_nan(RMq);
+        RMp = warp_max(RMp);
+        RMq = warp_max(RMq);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) flags |= __shfl_xor_sync(0xFFFFFFFFu, flags, o);
@@ -424,13 +459,11 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
     }
     double RSp = 0.0, RSq = 0.0;
     if (!GREEDY) {
-        // rescale each slice sum from its own max to the row max: S_c * 2^((M_c - M) c2)
+        // rescale each slice sum from its own scaled max to the row's: S_c * 2^(D_c - D)
         for (int cc = lane; cc < nch; cc += 32) {
             const PartA a = load_cg(parts + cc);
-            if (a.S_p > 0.0 && RMp < INFINITY)
-                RSp += a.S_p * exp2((static_cast<double>(a.M_p) - RMp) * P.c2d);
-            if (a.S_q > 0.0 && RMq < INFINITY)
-                RSq += a.S_q * exp2((static_cast<double>(a.M_q) - RMq) * P.c2d);
+            if (a.S_p > 0.0) RSp += a.S_p * exp2(static_cast<double>(a.M_p) - static_cast<double>(RMp));
+            if (a.S_q > 0.0) RSq += a.S_q * exp2(static_cast<double>(a.M_q) - static_cast<double>(RMq));
         }
         RSp = warp_sum(RSp);
         RSq = warp_sum(RSq);
@@ -441,11 +474,11 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
     bool stop = false;
     if (j < kk && (x < 0 || x >= P.V)) st = kBadId;
     if (!st) {
-        if ((flags & kPartNonfiniteP) || !(RMp < INFINITY)) st = kNonfinite;
+        if (flags & kPartNonfiniteP) st = kNonfinite;
         else if (RMp == -INFINITY) st = kEmptyRow;
     }
     if (!st && load_q) {
-        if ((flags & kPartNonfiniteQ) || !(RMq < INFINITY)) st = kNonfinite;
+        if (flags & kPartNonfiniteQ) st = kNonfinite;
         else if (RMq == -INFINITY) st = kEmptyRow;
     }
     if (st) {
@@ -457,11 +490,11 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
             st = kZeroQ;                                            // q_j(x_j) = 0 (C-7)
             stop = true;
         } else {
-            // log2 p_j(x_j) - log2 q_j(x_j), in fp64 on the kernel's own softmax scale
-            const double ell = (static_cast<double>(zxp) - RMp) * P.c2d - log2(RSp) -
-                               ((static_cast<double>(zxq) - RMq) * P.c2d - log2(RSq));
-            if (ell < 0.0) {                                        // a = min(1, p/q) < 1
-                const double a = exp2(ell);
+            // a = p(x)/q(x) = 2^((z_p(x) c2 - D_p) - (z_q(x) c2 - D_q)) * S_q / S_p
+            const double l = (static_cast<double>(zxp) * P.c2d - static_cast<double>(RMp)) -
+                             (static_cast<double>(zxq) * P.c2d - static_cast<double>(RMq));
+            const double a = exp2(l) * (RSq / RSp);
+            if (!(a >= 1.0)) {                                      // a = min(1, p/q) < 1
                 const uint4 w = verify_words(P.seed, static_cast<uint32_t>(j), P.round,
                                              P.rid_base + static_cast<uint64_t>(b));
                 stop = unit24(w.x) >= a;                            // reject iff u >= a (C-2)
@@ -481,21 +514,98 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
 
 // ------------------------------------------------------------------------------------------
 // Kernel B: residual (or bonus) inverse-CDF sample at the stop position L
+//
+// Residual terms of one 16-byte vector (raw bits of p and q), ascending token order:
+//   p(x) = 2^(z_p c2 - D_p) / S_p,  r(x) = max(0, p(x) - q(x)); r = p if !use_q.
+// Elements at or past `valid` are 0.  Returns the sequential fp32 sums of r and p (the order the
+// token search re-uses, so its partial sums are bit-identical).
+struct ResidParams {
+    float nDp, nDq, ip, iq;
+    int use_q;
+};
+template <typename E>
+__device__ __forceinline__ void resid_terms(uint4 up, uint4 uq, int valid, const ResidParams& rp,
+                                            float c2, float (&r)[Elt<E>::VEC],
+                                            float (&pv)[Elt<E>::VEC], float& sr, float& spv) {
+    using EL = Elt<E>;
+    constexpr int VEC = EL::VEC;
+    float v[VEC];
+    EL::unpack(up, v);
+    const unsigned long long cc = pk2(c2, c2), np = pk2(rp.nDp, rp.nDp);
+#pragma unroll
+    for (int u = 0; u < VEC; u += 2) {
+        float e0, e1;
+        upk2(ex2x2(ffma2(pk2(v[u], v[u + 1]), cc, np)), e0, e1);
+        pv[u] = __fmul_rn(e0, rp.ip);
+        pv[u + 1] = __fmul_rn(e1, rp.ip);
+    }
+    if (rp.use_q) {
+        float w[VEC];
+        EL::unpack(uq, w);
+        const unsigned long long nq = pk2(rp.nDq, rp.nDq);
+#pragma unroll
+        for (int u = 0; u < VEC; u += 2) {
+            float e0, e1;
+            upk2(ex2x2(ffma2(pk2(w[u], w[u + 1]), cc, nq)), e0, e1);
+            r[u] = fmaxf(__fsub_rn(pv[u], __fmul_rn(e0, rp.iq)), 0.0f);
+            r[u + 1] = fmaxf(__fsub_rn(pv[u + 1], __fmul_rn(e1, rp.iq)), 0.0f);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) r[u] = pv[u];
+    }
+#pragma unroll
+    for (int u = 0; u < VEC; ++u)
+        if (u >= valid) {
+            r[u] = 0.0f;
+            pv[u] = 0.0f;
+        }
+    sr = r[0];
+    spv = pv[0];
+#pragma unroll
+    for (int u = 1; u < VEC; ++u) {
+        sr = __fadd_rn(sr, r[u]);
+        spv = __fadd_rn(spv, pv[u]);
+    }
+}
+// inclusive Kogge-Stone scan of (R, P) pairs over the lanes (fixed association)
+__device__ __forceinline__ double2 warp_scan2(double2 v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double a = __shfl_up_sync(0xFFFFFFFFu, v.x, o);
+        const double b = __shfl_up_sync(0xFFFFFFFFu, v.y, o);
+        if (lane >= o) {
+            v.x = __dadd_rn(v.x, a);
+            v.y = __dadd_rn(v.y, b);
+        }
+    }
+    return v;
+}
+
+// grid (chunk c, request b).  CTA (c, b) stages chunk c of (p_L, q_L) (HBM; L2 when recent),
+// computes r and p per 32-vector segment (warp scans, fp64 segment masses) and the chunk's
+// masses (sequential over its segments).  The last CTA of request b searches chunk -> segment
+// -> token, recomputing the one segment with the identical routine.
 template <typename E>
 __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
     using EL = Elt<E>;
     constexpr int VEC = EL::VEC;
-    constexpr int TILE = kThreads * VEC;
-    constexpr int SEG = 32 * VEC;                 // tokens per warp segment
+    constexpr int SEGV = 32;                          // vectors per segment (one per lane)
+    constexpr int MAXSEG = kMaxChunkBytes / 16 / SEGV;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar;
-    __shared__ double2 s_seg[kMaxChunkBytes / kTileBytes * kWarps];
-    __shared__ double2 s_pb[256];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ double2 s_seg[MAXSEG];
     __shared__ int s_last;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nch = P.nch, kk = P.k;
-    const int c = blockIdx.x % nch, b = blockIdx.x / nch;
+    const int c = blockIdx.x, b = blockIdx.y + blockIdx.z * kGridY;
+    if (b >= P.B) return;   // (whole CTA: the request's tickets count only real CTAs)
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
     // programmatic dependent launch: this grid may start while k_row_stats drains; wait until
     // every row decision of the primary grid is complete and visible
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -505,99 +615,61 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
     const bool hard = (rs.status & kHard) != 0;
     const bool use_q = L < kk;
     const float c2 = P.c2;
-    const double invSp = 1.0 / rs.S_p;
-    const double invSq = use_q ? 1.0 / rs.S_q : 0.0;
-    const int nseg = P.nseg;
-    const E* gp = static_cast<const E*>(P.p) +
-                  (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
+    ResidParams rp;
+    rp.nDp = -rs.M_p;
+    rp.nDq = use_q ? -rs.M_q : 0.0f;
+    rp.ip = static_cast<float>(1.0 / rs.S_p);
+    rp.iq = use_q ? static_cast<float>(1.0 / rs.S_q) : 0.0f;
+    rp.use_q = use_q ? 1 : 0;
+    const E* gp = static_cast<const E*>(P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
     const E* gq = use_q ? static_cast<const E*>(P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q
                         : nullptr;
+    const int c0 = c * P.CH;
+    const int len = min(P.CH, P.V - c0);
+    const int nvv = (len + VEC - 1) / VEC;            // vectors incl. a ragged last one
+    const int nsg = (nvv + SEGV - 1) / SEGV;          // segments in this chunk
+    __syncthreads();
 
     if (!hard) {
-        const int c0 = c * P.CH;
-        const int len = min(P.CH, P.V - c0);
         E* sp = reinterpret_cast<E*>(smem);
         E* sq = sp + P.CH;
         const uint32_t bytes = static_cast<uint32_t>(len) * sizeof(E);
         const uint32_t bulk = bytes & ~15u;
         if (tid == 0) {
-            mbar_init(&bar, 1);
-            fence_mbar_init();
-        }
-        __syncthreads();
-        if (tid == 0) {
-            mbar_arrive_expect_tx(&bar, use_q ? 2u * bulk : bulk);
-            if (bulk) {
-                bulk_g2s(sp, gp + c0, bulk, &bar);
-                if (use_q) bulk_g2s(sq, gq + c0, bulk, &bar);
-            }
+            mbar_arrive_expect_tx(&bar[0], bulk);
+            if (bulk) bulk_g2s(sp, gp + c0, bulk, &bar[0]);
+        } else if (tid == 32 && use_q) {
+            mbar_arrive_expect_tx(&bar[1], bulk);
+            if (bulk) bulk_g2s(sq, gq + c0, bulk, &bar[1]);
         }
         for (int i = static_cast<int>(bulk / sizeof(E)) + tid; i < len; i += kThreads) {
             sp[i] = gp[c0 + i];
             if (use_q) sq[i] = gq[c0 + i];
         }
         __syncthreads();
-        mbar_wait(&bar, 0);
-
-        // warp w computes segments w*PER .. w*PER+PER-1 of the chunk (SEG contiguous tokens
-        // each); PER <= 4 independent Kogge-Stone scans run interleaved.  Segment totals are
-        // the scans' last lanes -- the same routine the final search re-runs on one segment.
-        const int PER = nseg / kWarps;
-        double vr[4], vpm[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            vr[i] = 0.0;
-            vpm[i] = 0.0;
-            const int e0 = (warp * PER + i) * SEG + lane * VEC;
-            if (i < PER && e0 < len) {
-                float vp[VEC], vq[VEC];
-                EL::unpack(*reinterpret_cast<const uint4*>(sp + e0), vp);
-                if (use_q) EL::unpack(*reinterpret_cast<const uint4*>(sq + e0), vq);
-                double r4 = 0.0, p4 = 0.0;
-#pragma unroll
-                for (int u = 0; u < VEC; ++u) {
-                    if (e0 + u < len) {
-                        const double pd = prob_term(vp[u], rs.M_p, c2, invSp);
-                        double rd = pd;
-                        if (use_q) {
-                            const double qd = prob_term(vq[u], rs.M_q, c2, invSq);
-                            rd = pd > qd ? __dsub_rn(pd, qd) : 0.0;
-                        }
-                        r4 = __dadd_rn(r4, rd);
-                        p4 = __dadd_rn(p4, pd);
-                    }
-                }
-                vr[i] = r4;
-                vpm[i] = p4;
+        mbar_wait(&bar[0], 0);
+        if (use_q) mbar_wait(&bar[1], 0);
+        for (int sg = warp; sg < nsg; sg += kWarps) {
+            const int g = sg * SEGV + lane;
+            const int valid = min(VEC, max(0, len - g * VEC));
+            uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
+            if (g < nvv) {
+                up = *reinterpret_cast<const uint4*>(sp + g * VEC);
+                if (use_q) uq = *reinterpret_cast<const uint4*>(sq + g * VEC);
             }
-        }
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const double nr = __shfl_up_sync(0xFFFFFFFFu, vr[i], o);
-                const double np = __shfl_up_sync(0xFFFFFFFFu, vpm[i], o);
-                if (lane >= o) {
-                    vr[i] = __dadd_rn(vr[i], nr);
-                    vpm[i] = __dadd_rn(vpm[i], np);
-                }
-            }
-        }
-        if (lane == 31) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (i < PER) s_seg[warp * PER + i] = make_double2(vr[i], vpm[i]);
+            float r[VEC], pv[VEC], sr, spv;
+            resid_terms<E>(up, uq, valid, rp, c2, r, pv, sr, spv);
+            const double2 inc = warp_scan2(make_double2(sr, spv), lane);
+            if (lane == 31) s_seg[sg] = inc;
         }
         __syncthreads();
-        double2* gseg = P.segtab + (static_cast<size_t>(b) * nch + c) * nseg;
-        for (int s = tid; s < nseg; s += kThreads) gseg[s] = s_seg[s];
-        if (tid == 0) {
-            double R = 0.0, Pm = 0.0;
-            for (int s = 0; s < nseg; ++s) {
-                R = __dadd_rn(R, s_seg[s].x);
-                Pm = __dadd_rn(Pm, s_seg[s].y);
-            }
-            P.partB[static_cast<size_t>(b) * nch + c] = PartB{R, Pm};
+        double2* gseg = P.segtab + (static_cast<size_t>(b) * nch + c) * P.nseg;
+        for (int sg = tid; sg < nsg; sg += kThreads) gseg[sg] = s_seg[sg];
+        if (warp == 0) {   // chunk masses: segment pairs, then a warp scan (the search's association)
+            const double2 a0 = 2 * lane < nsg ? s_seg[2 * lane] : make_double2(0.0, 0.0);
+            const double2 a1 = 2 * lane + 1 < nsg ? s_seg[2 * lane + 1] : make_double2(0.0, 0.0);
+            const double2 inc = warp_scan2(make_double2(__dadd_rn(a0.x, a1.x), __dadd_rn(a0.y, a1.y)), lane);
+            if (lane == 31) P.partB[static_cast<size_t>(b) * nch + c] = PartB{inc.x, inc.y};
         }
         __threadfence();
     }
@@ -614,125 +686,107 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
     int32_t status = rs.status;
     int32_t tok = -1;
     if (!hard) {
-        for (int cc = lane; cc < nch; cc += 32) {
-            const PartB pb = load_cg(P.partB + static_cast<size_t>(b) * nch + cc);
-            s_pb[cc] = make_double2(pb.R, pb.P);
+        // level 1: chunks, one lane each, warp scans over blocks of 32 chunks (carry between blocks)
+        auto chunk_mass = [&](int cc) -> double2 {
+            if (cc >= nch) return make_double2(0.0, 0.0);
+            const PartB t = load_cg(P.partB + static_cast<size_t>(b) * nch + cc);
+            return make_double2(t.R, t.P);
+        };
+        double2 carry = make_double2(0.0, 0.0);
+        for (int base = 0; base < nch; base += 32) {
+            const double2 icb = warp_scan2(chunk_mass(base + lane), lane);
+            carry.x = __dadd_rn(carry.x, __shfl_sync(0xFFFFFFFFu, icb.x, 31));
+            carry.y = __dadd_rn(carry.y, __shfl_sync(0xFFFFFFFFu, icb.y, 31));
         }
-        __syncwarp();
-        int cstar = 0, sstar = 0;
-        double th1 = 0.0;
-        bool zero_res = false;
-        if (lane == 0) {
-            double R = 0.0, Pm = 0.0;
-            for (int cc = 0; cc < nch; ++cc) {
-                R = __dadd_rn(R, s_pb[cc].x);
-                Pm = __dadd_rn(Pm, s_pb[cc].y);
+        const bool zero_res = use_q && !(carry.x > 0.0);        // C-6: fall back to p_L
+        const double tot = zero_res ? carry.y : carry.x;
+        const uint4 w = verify_words(P.seed, static_cast<uint32_t>(L), P.round,
+                                     P.rid_base + static_cast<uint64_t>(b));
+        const double theta = unit24(w.y) * tot;                 // C-9: first x with C(x) > theta
+        int cstar = -1, clast = 0;
+        double th1 = INFINITY, run = 0.0;
+        for (int base = 0; base < nch && cstar < 0; base += 32) {
+            const double2 pb = chunk_mass(base + lane);
+            const double2 icb = warp_scan2(pb, lane);
+            const double icm = __dadd_rn(run, zero_res ? icb.y : icb.x);
+            const double mcm = zero_res ? pb.y : pb.x;
+            const unsigned h = __ballot_sync(0xFFFFFFFFu, base + lane < nch && icm > theta);
+            const unsigned pm = __ballot_sync(0xFFFFFFFFu, base + lane < nch && mcm > 0.0);
+            if (pm) clast = base + 31 - __clz(pm);
+            if (h) {
+                const int l = __ffs(h) - 1;
+                double e = __shfl_up_sync(0xFFFFFFFFu, icm, 1);
+                if (lane == 0) e = run;
+                cstar = base + l;
+                th1 = theta - __shfl_sync(0xFFFFFFFFu, e, l);
             }
-            zero_res = use_q && !(R > 0.0);                 // C-6: fall back to p_L
-            const double tot = zero_res ? Pm : R;
-            const uint4 w = verify_words(P.seed, static_cast<uint32_t>(L), P.round,
-                                         P.rid_base + static_cast<uint64_t>(b));
-            const double theta = unit24(w.y) * tot;
-            double run = 0.0;
-            cstar = -1;
-            int lastpos = 0;
-            for (int cc = 0; cc < nch; ++cc) {
-                const double m = zero_res ? s_pb[cc].y : s_pb[cc].x;
-                if (m > 0.0) lastpos = cc;
-                const double nr = __dadd_rn(run, m);
-                if (nr > theta) {
-                    cstar = cc;
-                    break;
-                }
-                run = nr;
-            }
-            if (cstar < 0) {          // rounding: clamp to the last chunk with mass (C-9)
-                cstar = lastpos;
-                th1 = INFINITY;
-            } else {
-                th1 = theta - run;
-            }
+            run = __shfl_sync(0xFFFFFFFFu, icm, 31);
         }
-        cstar = __shfl_sync(0xFFFFFFFFu, cstar, 0);
-        th1 = __shfl_sync(0xFFFFFFFFu, th1, 0);
-        zero_res = __shfl_sync(0xFFFFFFFFu, static_cast<int>(zero_res), 0) != 0;
-        const double2* gseg = P.segtab + (static_cast<size_t>(b) * nch + cstar) * nseg;
-        for (int s = lane; s < nseg; s += 32) s_seg[s] = __ldcg(gseg + s);
-        __syncwarp();
-        double th2 = 0.0;
-        if (lane == 0) {
-            double run = 0.0;
-            sstar = -1;
-            int lastpos = 0;
-            for (int s = 0; s < nseg; ++s) {
-                const double m = zero_res ? s_seg[s].y : s_seg[s].x;
-                if (m > 0.0) lastpos = s;
-                const double nr = __dadd_rn(run, m);
-                if (nr > th1) {
-                    sstar = s;
-                    break;
-                }
-                run = nr;
-            }
-            if (sstar < 0) {
-                sstar = lastpos;
-                th2 = INFINITY;
-            } else {
-                th2 = th1 - run;
-            }
-        }
-        sstar = __shfl_sync(0xFFFFFFFFu, sstar, 0);
-        th2 = __shfl_sync(0xFFFFFFFFu, th2, 0);
-        // re-read the segment's 32*VEC tokens and scan them exactly as the main pass did
-        const int base = cstar * P.CH + (sstar / kWarps) * TILE + (sstar % kWarps) * SEG;
-        const int my0 = base + lane * VEC;
-        double rv[VEC];
-        double r4 = 0.0;
-#pragma unroll
-        for (int u = 0; u < VEC; ++u) {
-            rv[u] = 0.0;
-            const int xx = my0 + u;
-            if (xx < P.V && xx < (cstar + 1) * P.CH) {
-                const double pd = prob_term(EL::one(gp, xx), rs.M_p, c2, invSp);
-                double rd = pd;
-                if (use_q && !zero_res) {
-                    const double qd = prob_term(EL::one(gq, xx), rs.M_q, c2, invSq);
-                    rd = pd > qd ? __dsub_rn(pd, qd) : 0.0;
-                }
-                rv[u] = rd;
-            }
-            r4 = __dadd_rn(r4, rv[u]);
-        }
-        const double incl = warp_incl_scan(r4, lane);
-        double excl = __shfl_up_sync(0xFFFFFFFFu, incl, 1);
-        if (lane == 0) excl = 0.0;
-        const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl > th2);
-        int fl, fu = -1;
-        if (hit) {
-            fl = __ffs(hit) - 1;
-            if (lane == fl) {
-                double run = excl;
-                int lastpos = -1;
-#pragma unroll
-                for (int u = 0; u < VEC; ++u) {
-                    if (rv[u] > 0.0) lastpos = u;
-                    run = __dadd_rn(run, rv[u]);
-                    if (fu < 0 && run > th2) fu = u;
-                }
-                if (fu < 0) fu = lastpos;
-            }
+        if (cstar < 0) cstar = clast;                           // rounding: last chunk with mass
+        // level 2: segments of chunk cstar (pairs per lane, warp scan: the main pass's association)
+        const int cl = min(P.CH, P.V - cstar * P.CH);
+        const int cnvv = (cl + VEC - 1) / VEC;
+        const int cnsg = (cnvv + SEGV - 1) / SEGV;
+        const double2* gseg = P.segtab + (static_cast<size_t>(b) * nch + cstar) * P.nseg;
+        const double2 a0 = 2 * lane < cnsg ? __ldcg(gseg + 2 * lane) : make_double2(0.0, 0.0);
+        const double2 a1 = 2 * lane + 1 < cnsg ? __ldcg(gseg + 2 * lane + 1) : make_double2(0.0, 0.0);
+        const double m0 = zero_res ? a0.y : a0.x, m1 = zero_res ? a1.y : a1.x;
+        const double2 ip = warp_scan2(make_double2(__dadd_rn(a0.x, a1.x), __dadd_rn(a0.y, a1.y)), lane);
+        const double ipm = zero_res ? ip.y : ip.x;
+        const unsigned hs = __ballot_sync(0xFFFFFFFFu, ipm > th1);
+        const unsigned ps = __ballot_sync(0xFFFFFFFFu, __dadd_rn(m0, m1) > 0.0);
+        const int lp = hs ? __ffs(hs) - 1 : (ps ? 31 - __clz(ps) : 0);
+        double exs = __shfl_up_sync(0xFFFFFFFFu, ipm, 1);
+        if (lane == 0) exs = 0.0;
+        exs = __shfl_sync(0xFFFFFFFFu, exs, lp);
+        const double lm0 = __shfl_sync(0xFFFFFFFFu, m0, lp), lm1 = __shfl_sync(0xFFFFFFFFu, m1, lp);
+        int sstar;
+        double th2;
+        if (!hs) {                                    // rounding: last segment with mass
+            sstar = lm1 > 0.0 ? 2 * lp + 1 : 2 * lp;
+            th2 = INFINITY;
+        } else if (__dadd_rn(exs, lm0) > th1) {
+            sstar = 2 * lp;
+            th2 = th1 - exs;
         } else {
-            // rounding: the last token of the segment with positive mass
-            int lastpos = -1;
-#pragma unroll
-            for (int u = 0; u < VEC; ++u)
-                if (rv[u] > 0.0) lastpos = u;
-            const unsigned pos = __ballot_sync(0xFFFFFFFFu, lastpos >= 0);
-            fl = pos ? 31 - __clz(pos) : 0;
-            if (lane == fl) fu = lastpos >= 0 ? lastpos : 0;
+            sstar = 2 * lp + 1;
+            th2 = th1 - __dadd_rn(exs, lm0);
         }
-        fu = __shfl_sync(0xFFFFFFFFu, fu, fl);
-        tok = base + fl * VEC + fu;
+        // recompute the segment exactly as the main pass did (r and p terms both; zero_res
+        // selects p)
+        const int g = sstar * SEGV + lane;
+        const int valid = min(VEC, max(0, cl - g * VEC));
+        uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
+        if (g < cnvv) {
+            up = __ldcg(reinterpret_cast<const uint4*>(gp + cstar * P.CH) + g);
+            if (use_q) uq = __ldcg(reinterpret_cast<const uint4*>(gq + cstar * P.CH) + g);
+        }
+        float r[VEC], pv[VEC], sr, spv;
+        resid_terms<E>(up, uq, valid, rp, c2, r, pv, sr, spv);
+        const double2 inc = warp_scan2(make_double2(sr, spv), lane);
+        const double icv = zero_res ? inc.y : inc.x;
+        const float mine = zero_res ? spv : sr;
+        const unsigned hit = __ballot_sync(0xFFFFFFFFu, icv > th2);
+        const unsigned posm = __ballot_sync(0xFFFFFFFFu, mine > 0.0f);
+        const int ls = hit ? __ffs(hit) - 1 : (posm ? 31 - __clz(posm) : 0);
+        double ex = __shfl_up_sync(0xFFFFFFFFu, icv, 1);
+        if (lane == 0) ex = 0.0;
+        int fe = -1;
+        if (lane == ls) {
+            const double th3 = hit ? th2 - ex : INFINITY;
+            int lastpos = -1;
+            float cum = 0.0f;
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                const float te = zero_res ? pv[e] : r[e];
+                if (te > 0.0f) lastpos = e;
+                cum = e == 0 ? te : __fadd_rn(cum, te);
+                if (fe < 0 && static_cast<double>(cum) > th3) fe = e;
+            }
+            if (fe < 0) fe = lastpos >= 0 ? lastpos : 0;   // rounding: clamp (C-9)
+        }
+        fe = __shfl_sync(0xFFFFFFFFu, fe, ls);
+        tok = cstar * P.CH + (sstar * SEGV + ls) * VEC + fe;
         if (zero_res) status |= kZeroResidual;
     }
     if (lane == 0) {
@@ -787,10 +841,10 @@ __global__ void k_philox(uint64_t seed, uint64_t round, const uint32_t* pos, con
 // Second kernel of a call: programmatic dependent launch, so its launch and prologue overlap the
 // tail of k_row_stats (the kernel waits with griddepcontrol.wait before reading decisions).
 template <typename K>
-static cudaError_t launch_dependent(K kernel, unsigned grid, unsigned block, size_t smem,
+static cudaError_t launch_dependent(K kernel, dim3 grid, unsigned block, size_t smem,
                                     cudaStream_t st, const Params& P) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = grid;
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -826,13 +880,15 @@ static cudaError_t launch_sampled(const Params& P, cudaStream_t st, cudaEvent_t 
 
         attr = true;
     }
-    const unsigned gridA = static_cast<unsigned>(P.k + 1) * P.B * P.nch;
+    const int nb = (P.B + kGridY - 1) / kGridY;
+    const dim3 gridA(P.nch, P.B < kGridY ? P.B : kGridY, (P.k + 1) * nb);
     record_event(ev0, st);
     k_row_stats<E, false><<<gridA, kThreads, smem, st>>>(P);
     record_event(ev1, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return launch_dependent(k_sample<E>, static_cast<unsigned>(P.B) * P.nch, kThreads, smem, st, P);
+    return launch_dependent(k_sample<E>, dim3(P.nch, P.B < kGridY ? P.B : kGridY, nb), kThreads, smem,
+                            st, P);
 }
 
 template <typename E>
@@ -845,13 +901,14 @@ static cudaError_t launch_greedy(const Params& P, cudaStream_t st, cudaEvent_t e
                              kMaxChunkBytes * 2);
         attr = true;
     }
-    const unsigned gridA = static_cast<unsigned>(P.k + 1) * P.B * P.nch;
+    const int nb = (P.B + kGridY - 1) / kGridY;
+    const dim3 gridA(P.nch, P.B < kGridY ? P.B : kGridY, (P.k + 1) * nb);
     record_event(ev0, st);
     k_row_stats<E, true><<<gridA, kThreads, smem, st>>>(P);
     record_event(ev1, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return launch_dependent(k_finalize_greedy, (P.B + 127) / 128, 128, 0, st, P);
+    return launch_dependent(k_finalize_greedy, dim3((P.B + 127) / 128), 128, 0, st, P);
 }
 
 cudaError_t launch_verify(const Params& P, bool greedy, bool bf16, cudaStream_t st,
