@@ -302,10 +302,10 @@ def run_ours(args):
     (ms_max,), (tokens_all,) = reduce_max_sum([ms], [tokens], dev)
     value = tokens_all / (ms_max / 1000.0)
 
-    # dominant kernel (the cluster kernel, or k_row_stats on the two-launch path): algorithmic
+    # dominant kernel (k_row_stats on the two-launch path; the stream variant's kernel): algorithmic
     # bytes of the whole step per launch / its CUDA-event time on the launching stream
     pl = sd.plan(B, k, V, T, torch.float32 if args.dtype == "f32" else torch.bfloat16)
-    kname = {"stream": "k_verify_stream", "cluster": "k_verify_cluster"}.get(pl["variant"], "k_row_stats")
+    kname = "k_verify_stream" if pl["variant"] == "stream" else "k_row_stats"
     kA_mean_ms = statistics.fmean(kA)
     alg_per_launch = alg / K
     peak, peak_kind = load_peaks()

@@ -117,26 +117,22 @@ sd_status sd_verify_workspace_size(const sd_shape* shape, float temperature, siz
 /*
  * sd_verify_plan -- how sd_verify will run this shape on the current device (host only; it
  * may query the device's occupancy limits, but launches nothing).
- *   variant      SD_VARIANT_TWO_LAUNCH (default): k_row_stats + k_sample / k_finalize_greedy;
- *                SD_VARIANT_STREAM: one launch of `ctas` persistent CTAs in clusters of
- *                `cluster`; each CTA streams a `slice`-logit vocabulary slice of every row pair
- *                its cluster owns through a TMA ring (every reached logit read from HBM once);
- *                SD_VARIANT_CLUSTER: one launch, (k+1)*B thread-block clusters of `cluster`
- *                CTAs, each CTA holding a `slice`-logit slice of a (p_j, q_j) row pair in shared
- *                memory (every logit read from HBM at most once);
- *                SD_VARIANT_FUSED: one persistent cooperative launch.
+ *   variant      SD_VARIANT_TWO_LAUNCH (default): k_row_stats (grid = chunk x request x position,
+ *                position-major) + k_sample / k_finalize_greedy, PDL-chained;
+ *                SD_VARIANT_STREAM (STARSD_KERNEL=stream, when the shape fits): one launch of `ctas`
+ *                persistent CTAs in clusters of `cluster`, each streaming a `slice`-logit slice of
+ *                every row pair its cluster owns through a TMA ring
  *   launches     kernel launches per sd_verify call
- *   cluster, slice, ctas   cluster size, logits per CTA slice, CTAs in the (first) launch
- *   max_active_clusters, smem_bytes   occupancy of the cluster variant (0 otherwise)
- * Environment STARSD_KERNEL=stream|cluster|fused selects another variant (default: two-launch;
- * a variant that cannot serve a shape falls back to the two-launch path).
+ *   cluster, slice, ctas   cluster size (0: none), logits per CTA slice / chunk, CTAs in the first
+ *                launch
+ *   max_active_clusters, smem_bytes   occupancy of the stream variant (0 otherwise)
  */
-enum { SD_VARIANT_CLUSTER = 0, SD_VARIANT_TWO_LAUNCH = 1, SD_VARIANT_FUSED = 2, SD_VARIANT_STREAM = 3 };
+enum { SD_VARIANT_TWO_LAUNCH = 1, SD_VARIANT_STREAM = 3 };
 typedef struct {
     int32_t variant, launches, cluster, slice;
     int64_t ctas;
-    int32_t max_active_clusters;   /* cluster variant: clusters the device keeps resident */
-    int32_t smem_bytes;            /* dynamic shared memory per CTA                        */
+    int32_t max_active_clusters;   /* stream variant: clusters the device keeps resident */
+    int32_t smem_bytes;            /* stream variant: dynamic shared memory per CTA       */
 } sd_plan;
 sd_status sd_verify_plan(const sd_shape* shape, float temperature, sd_plan* out);
 
@@ -153,7 +149,8 @@ sd_status sd_philox_uniforms(uint64_t seed, uint64_t round, const uint32_t* pos,
 /*
  * sd_profile_events -- tracing hook for benchmarks.  After this call, the next n_pairs
  * sd_verify calls on this thread record events[2 i] immediately before and events[2 i + 1]
- * immediately after their stats kernel (k_row_stats, the HBM-streaming kernel), on the call's
+ * immediately after their dominant kernel (k_row_stats, the HBM-streaming kernel, or the stream
+ * variant's single kernel), on the call's
  * stream (graph capture records them as event nodes).  events: host array of 2 * n_pairs
  * caller-created cudaEvent_t handles; n_pairs = 0 disables.  The caller reads the durations
  * with cudaEventElapsedTime.
@@ -161,10 +158,12 @@ sd_status sd_philox_uniforms(uint64_t seed, uint64_t round, const uint32_t* pos,
 sd_status sd_profile_events(cudaEvent_t* events, int32_t n_pairs);
 
 /*
- * sd_debug_trace -- development timeline.  When device_buf != NULL, subsequent sd_verify calls
- * on this thread write %globaltimer stamps (ns) into it: [4 * grid] per-CTA start / producer
- * phase-1 end / producer end / CTA exit, then [B*(k+1)] row-decision times, [B*(k+1)]
- * sampling-pass end times, [B] request completion times.  NULL disables.
+ * sd_debug_trace -- development instrumentation of the stream variant (library built with
+ * STARSD_BUILD_DEBUG=1; otherwise ignored).  When device_buf != NULL, subsequent stream-variant
+ * sd_verify calls on this thread write, per CTA, a record log of kSTraceN = 8192 uint64 words:
+ * word 0 = record count, then event records (type << 56 | arg << 40 | %globaltimer), and the
+ * last 16 words = clock64 accounting counters (tools/trace_stream.py, tools/analyze_strace.py).
+ * NULL disables.
  */
 sd_status sd_debug_trace(unsigned long long* device_buf);
 

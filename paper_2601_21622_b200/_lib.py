@@ -36,7 +36,7 @@ class Plan(ctypes.Structure):
                 ("max_active_clusters", ctypes.c_int32), ("smem_bytes", ctypes.c_int32)]
 
 
-VARIANT_NAMES = {0: "cluster", 1: "two_launch", 2: "fused", 3: "stream"}
+VARIANT_NAMES = {1: "two_launch", 3: "stream"}
 
 
 class StarConfig(ctypes.Structure):

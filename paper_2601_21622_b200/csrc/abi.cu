@@ -16,7 +16,6 @@
 namespace sd {
 cudaError_t launch_verify(const Params& P, bool greedy, bool bf16, cudaStream_t st,
                           cudaEvent_t ev0, cudaEvent_t ev1);
-cudaError_t launch_fused(const fused::FParams& P, bool greedy, bool bf16, cudaStream_t st);
 cudaError_t launch_philox(uint64_t seed, uint64_t round, const uint32_t* pos, const uint64_t* rid,
                           int n, uint32_t* out, cudaStream_t st);
 
@@ -36,19 +35,15 @@ void clear_error() { g_err[0] = '\0'; }
 const char* last_error() { return g_err; }
 
 // Kernel variant.  Default: the two-launch path (verify_kernels.cu: k_row_stats + k_sample /
-// k_finalize_greedy, PDL-chained), measured fastest on B200 for every BASELINE config this round.
-// STARSD_KERNEL=stream / cluster / fused select the persistent warp-specialized cluster kernel
-// (verify_stream.cu), the row-holding cluster kernel (verify_cluster.cu) or the persistent
-// cooperative kernel (verify_fused.cu): cross-variant parity checks and study.
-enum Variant { kCluster = 0, kTwoLaunch = 1, kFused = 2, kStream = 3 };
+// k_finalize_greedy, PDL-chained), measured fastest on B200 for every BASELINE config.
+// STARSD_KERNEL=stream selects the persistent warp-specialized cluster kernel (verify_stream.cu)
+// when the shape fits it: a cross-variant parity check and design study.
+enum Variant { kTwoLaunch = 1, kStream = 3 };
 static Variant variant() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("STARSD_KERNEL");
-        v = kTwoLaunch;
-        if (e && strcmp(e, "stream") == 0) v = kStream;
-        if (e && strcmp(e, "cluster") == 0) v = kCluster;
-        if (e && strcmp(e, "fused") == 0) v = kFused;
+        v = (e && strcmp(e, "stream") == 0) ? kStream : kTwoLaunch;
     }
     return static_cast<Variant>(v);
 }
@@ -56,23 +51,15 @@ static Variant variant() {
 bool stream_config(int32_t V, int esz, bool greedy, StreamPlan* out);
 cudaError_t launch_stream(const SParams& P, bool greedy, bool bf16, size_t smem, cudaStream_t st,
                           cudaEvent_t ev0, cudaEvent_t ev1);
-bool cluster_config(int32_t V, int esz, bool greedy, int32_t* C, int32_t* W, int32_t* nvr,
-                    size_t* smem);
-int cluster_max_active(int32_t V, int esz, bool greedy);
-cudaError_t launch_cluster(const CParams& P, bool greedy, bool bf16, size_t smem, cudaStream_t st,
-                           cudaEvent_t ev0, cudaEvent_t ev1);
 
 void record_event(cudaEvent_t ev, cudaStream_t st);
 
-// the fused kernel serves at most kFusedMaxBatch requests per launch; sd_verify splits larger
-// batches into consecutive launches on the same stream (the workspace is reused in order)
-constexpr int32_t kFusedMaxBatch = 4096;
-
+// The stream kernel uses a prefix of the two-launch layout (rej_mask, ticketB, rowstat).
 static size_t ws_bytes(int32_t B, int32_t k, int32_t V, int32_t esz) {
-    const int32_t Bl = B < kFusedMaxBatch ? B : kFusedMaxBatch;
-    const size_t a = ws_layout(B, k, V, esz).total, b = fused_layout(Bl, k, V, esz).total;
-    return a > b ? a : b;
+    return ws_layout(B, k, V, esz).total;
 }
+
+constexpr int32_t kMaxVocab = 1 << 24;
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -97,9 +84,9 @@ sd_status check_shape(const sd_shape* s, float T, int* esz) {
     if (!(T == 0.0f || (std::isfinite(T) && T >= 1e-3f)))
         return fail(SD_ERR_INVALID_ARGUMENT, "temperature=%g must be 0 or finite >= 1e-3",
                     (double)T);
-    if (s->vocab > fused_max_vocab(*esz))
+    if (s->vocab > kMaxVocab)
         return fail(SD_ERR_UNSUPPORTED, "vocab=%d too large for this build (max %d)", s->vocab,
-                    fused_max_vocab(*esz));
+                    kMaxVocab);
     const int64_t rows = (int64_t)(s->k + 1) * s->batch;
     if (rows >= (1LL << 31)) return fail(SD_ERR_UNSUPPORTED, "batch=%d too large", s->batch);
     return SD_OK;
@@ -153,65 +140,6 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     // c2 = log2(e) / T rounded to fp32; every exponent in the kernels uses this one constant
     const float c2 =
         greedy ? 0.0f : static_cast<float>(1.4426950408889634 / static_cast<double>(temperature));
-    if (variant() == kFused) {
-        const int32_t esz_ = esz;
-        for (int32_t off = 0; off < shape->batch; off += kFusedMaxBatch) {
-            const int32_t Bl = shape->batch - off < kFusedMaxBatch ? shape->batch - off : kFusedMaxBatch;
-            const FusedLayout w = fused_layout(Bl, shape->k, shape->vocab, esz_);
-            const int64_t ldp = shape->ld_p ? shape->ld_p : shape->vocab;
-            const int64_t ldq = shape->ld_q ? shape->ld_q : shape->vocab;
-            fused::FParams F{};
-            F.p = static_cast<const char*>(p_logits) + (size_t)off * (shape->k + 1) * ldp * esz_;
-            F.q = greedy ? nullptr
-                         : static_cast<const char*>(q_logits) + (size_t)off * shape->k * ldq * esz_;
-            F.ids = draft_ids + (size_t)off * shape->k;
-            F.B = Bl;
-            F.k = shape->k;
-            F.V = shape->vocab;
-            F.ld_p = ldp;
-            F.ld_q = ldq;
-            F.nch = w.nch;
-            F.CHI = w.CHI;
-            F.n_items = (shape->k + 1) * Bl * w.nch;
-            F.c2 = c2;
-            F.c2d = static_cast<double>(c2);
-            F.seed = seed;
-            F.round = round;
-            F.rid_base = request_id_base + static_cast<uint64_t>(off);
-            F.out_L = out_accept_len + off;
-            F.out_tok = out_tokens + (size_t)off * (shape->k + 1);
-            F.out_status = out_status ? out_status + off : nullptr;
-            char* ws = static_cast<char*>(workspace);
-            F.evt = reinterpret_cast<uint32_t*>(ws + w.evt);
-            F.stop = reinterpret_cast<uint32_t*>(ws + w.stop);
-            F.ticketA = reinterpret_cast<uint32_t*>(ws + w.ticketA);
-            F.ticketB = reinterpret_cast<uint32_t*>(ws + w.ticketB);
-            F.glob = reinterpret_cast<uint32_t*>(ws + w.glob);
-            F.mbox_tail = reinterpret_cast<uint32_t*>(ws + w.mbox_tail);
-            F.mbox = reinterpret_cast<uint32_t*>(ws + w.mbox);
-            F.mcap = w.mcap;
-            F.rowstat = reinterpret_cast<RowStat*>(ws + w.rowstat);
-            F.cand = reinterpret_cast<int2*>(ws + w.cand);
-            F.partA = reinterpret_cast<PartA*>(ws + w.partA);
-            F.partB = reinterpret_cast<PartB*>(ws + w.partB);
-            F.segtab = reinterpret_cast<double2*>(ws + w.segtab);
-            F.trace = g_trace;
-            {
-                static int dbg = -1;
-                if (dbg < 0) {
-                    const char* e = getenv("STARSD_DEBUG");
-                    dbg = e ? atoi(e) : 0;
-                }
-                F.debug = dbg;
-            }
-            if (off == 0) record_event(ev0, stream);
-            cudaError_t e = launch_fused(F, greedy, shape->dtype == SD_DTYPE_BF16, stream);
-            if (e != cudaSuccess)
-                return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
-        }
-        record_event(ev1, stream);
-        return SD_OK;
-    }
     const WsLayout w = ws_layout(shape->batch, shape->k, shape->vocab, esz);
     char* ws = static_cast<char*>(workspace);
     StreamPlan sp;
@@ -253,36 +181,6 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
         if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
         return SD_OK;
     }
-    int32_t cC, cW, cnvr;
-    size_t csmem;
-    if (variant() == kCluster && cluster_config(shape->vocab, esz, greedy, &cC, &cW, &cnvr, &csmem)) {
-        CParams C{};
-        C.p = p_logits;
-        C.q = greedy ? nullptr : q_logits;
-        C.ids = draft_ids;
-        C.B = shape->batch;
-        C.k = shape->k;
-        C.V = shape->vocab;
-        C.ld_p = shape->ld_p ? shape->ld_p : shape->vocab;
-        C.ld_q = shape->ld_q ? shape->ld_q : shape->vocab;
-        C.C = cC;
-        C.W = cW;
-        C.nvr = cnvr;
-        C.c2 = c2;
-        C.seed = seed;
-        C.round = round;
-        C.rid_base = request_id_base;
-        C.out_L = out_accept_len;
-        C.out_tok = out_tokens;
-        C.out_status = out_status;
-        C.rej_mask = reinterpret_cast<uint32_t*>(ws + w.rej_mask);
-        C.ticket = reinterpret_cast<uint32_t*>(ws + w.ticketB);
-        C.rowres = reinterpret_cast<int2*>(ws + w.rowstat);
-        cudaError_t e = launch_cluster(C, greedy, shape->dtype == SD_DTYPE_BF16, csmem, stream, ev0, ev1);
-        if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
-        return SD_OK;
-    }
-
     Params P{};
     P.p = p_logits;
     P.q = greedy ? nullptr : q_logits;
@@ -322,8 +220,6 @@ sd_status sd_verify_plan(const sd_shape* shape, float temperature, sd_plan* out)
     if (s != SD_OK) return s;
     if (!out) return fail(SD_ERR_INVALID_ARGUMENT, "out is NULL");
     const bool greedy = temperature == 0.0f;
-    int32_t cC, cW, cnvr;
-    size_t csmem;
     *out = sd_plan{};
     StreamPlan sp;
     if (variant() == kStream && stream_config(shape->vocab, esz, greedy, &sp)) {
@@ -334,21 +230,6 @@ sd_status sd_verify_plan(const sd_shape* shape, float temperature, sd_plan* out)
         out->ctas = (int64_t)sp.G * sp.C;
         out->max_active_clusters = sp.G;
         out->smem_bytes = (int32_t)sp.smem;
-        return SD_OK;
-    }
-    if (variant() == kCluster && cluster_config(shape->vocab, esz, greedy, &cC, &cW, &cnvr, &csmem)) {
-        out->variant = SD_VARIANT_CLUSTER;
-        out->launches = 1;
-        out->cluster = cC;
-        out->slice = cW;
-        out->ctas = (int64_t)(shape->k + 1) * shape->batch * cC;
-        out->max_active_clusters = cluster_max_active(shape->vocab, esz, greedy);
-        out->smem_bytes = (int32_t)csmem;
-        return SD_OK;
-    }
-    if (variant() == kFused) {
-        out->variant = SD_VARIANT_FUSED;
-        out->launches = (shape->batch + kFusedMaxBatch - 1) / kFusedMaxBatch;
         return SD_OK;
     }
     int32_t nch, CH;

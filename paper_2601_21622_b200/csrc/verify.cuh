@@ -10,7 +10,7 @@ constexpr int kThreads = 256;            // threads per CTA (8 warps)
 constexpr int kWarps = kThreads / 32;
 constexpr int kVecBytes = 16;            // one 128-bit smem/global vector per thread per tile
 constexpr int kTileBytes = kThreads * kVecBytes;   // 4 KB of one row per tile
-constexpr int kMaxChunkBytes = 32 * 1024;          // one CTA owns <= 32 KB of a row
+constexpr int kMaxChunkBytes = 16 * 1024;          // one CTA owns <= 16 KB of a row (measured best of 8/16/32 KB)
                                                    // (one 32 KB bulk copy per row and CTA)
 
 // Per (request b, position j, vocab chunk c): what one kernel-A CTA found in its slice.
@@ -100,30 +100,7 @@ inline WsLayout ws_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
     return w;
 }
 
-// ---- cluster (v3) kernel: one thread-block cluster per (request, position) row pair --------
-constexpr int kCThreads = 256;      // threads per CTA
-constexpr int kCMaxPieces = 14;     // 16 KB bulk copies per row slice (<= 224 KB)
-
-struct CParams {
-    const void* p;
-    const void* q;
-    const int32_t* ids;
-    int32_t B, k, V;
-    int64_t ld_p, ld_q;          // elements
-    int32_t C;                   // CTAs per cluster (1..16)
-    int32_t W;                   // vocabulary slice per CTA (elements, multiple of 16 bytes)
-    int32_t nvr;                 // 16-byte vectors per thread in the residual pass (odd)
-    float c2;                    // log2(e) / T in fp32 (0 for greedy)
-    uint64_t seed, round, rid_base;
-    int32_t* out_L;
-    int32_t* out_tok;
-    int32_t* out_status;
-    uint32_t* rej_mask;          // [B] bit j: position j stopped the chain (zero region)
-    uint32_t* ticket;            // [B] rows of the request finished (zero region)
-    int2* rowres;                // [B][k+1] (token, status) of a stopping / bonus row
-};
-
-// ---- stream (v4) kernel: persistent warp-specialized clusters --------------------------------
+// ---- stream kernel (opt-in): persistent warp-specialized clusters --------------------------------
 constexpr int kSStatsWarps = 8;
 constexpr int kSRowWarps = 4;
 constexpr int kSProducers = 2;             // producer lanes issuing main-ring copies (tools/tma_probe:
@@ -165,85 +142,5 @@ struct StreamPlan {
     int32_t C, G, W, segmax, nslot;
     size_t smem;
 };
-
-// ---- fused (v2) kernel: parameters and workspace layout ----------------------------------
-namespace fused {
-constexpr int kRowChunkBytesH = 16384;    // must equal fused::kRowChunkBytes in verify_fused.cu
-constexpr int kSegsH = 32;
-struct FParams {
-    const void* p;
-    const void* q;
-    const int32_t* ids;
-    int32_t B, k, V;
-    int64_t ld_p, ld_q;
-    int32_t nch, CHI;      // chunks per row, elements per chunk
-    int32_t n_items;       // (k+1) * B * nch phase-1 items
-    float c2;              // log2(e)/T in fp32
-    double c2d;            // the same value in fp64
-    uint64_t seed, round, rid_base;
-    int32_t* out_L;
-    int32_t* out_tok;
-    int32_t* out_status;
-    // zero-filled workspace region (left zero by every call)
-    uint32_t* evt;         // [B] rows_done | spawned << 8 | resid_done << 16
-    uint32_t* stop;        // [B] bit j: position j stops the chain (rejection or fault)
-    uint32_t* ticketA;     // [B*(k+1)] phase-1 chunk arrivals (skips in the high half)
-    uint32_t* ticketB;     // [B*(k+1)] phase-2 chunk arrivals
-    uint32_t* glob;        // [4] (unused), (unused), finished requests, exited CTAs
-    uint32_t* mbox_tail;   // [max grid] per-CTA mailbox fill counters
-    uint32_t* mbox;        // [max grid][mcap] per-CTA mailboxes of phase-2 work entries
-    int32_t mcap;
-    // scratch
-    RowStat* rowstat;      // [B*(k+1)]
-    int2* cand;            // [B*(k+1)] candidate token + informational status of a pass
-    PartA* partA;          // [B*(k+1)*nch]
-    PartB* partB;          // [B*(k+1)*nch]
-    double2* segtab;       // [B*(k+1)*nch*kSegs]
-    // optional debug timeline (nullptr in production): globaltimer stamps, see sd_debug_trace
-    unsigned long long* trace;
-    // development bisection knobs (0 in production): bit0 stream only (no requests complete;
-    // the kernel ends after phase 1), bit1 consumers skip the arithmetic, bit2 epilogue skips
-    // global traffic, bit3 producer ignores stop masks (no laziness)
-    int32_t debug;
-};
-
-}  // namespace fused
-
-constexpr int kFusedMaxGrid = 1024;
-constexpr int kFusedMinGrid = 64;
-
-struct FusedLayout {
-    size_t evt, stop, ticketA, ticketB, glob, mbox_tail, mbox, zero_bytes;
-    size_t rowstat, cand, partA, partB, segtab, total;
-    int32_t nch, CHI, mcap;
-};
-
-inline FusedLayout fused_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
-    FusedLayout w{};
-    w.CHI = fused::kRowChunkBytesH / esz;
-    w.nch = (V + w.CHI - 1) / w.CHI;
-    const size_t rows = static_cast<size_t>(B) * (k + 1);
-    // a sampling pass puts ceil(nch / grid) entries in each of min(nch, grid) mailboxes and
-    // every row sends at most one decider message; the kernel requires grid >= kFusedMinGrid
-    w.mcap = static_cast<int32_t>(rows * ((w.nch + kFusedMinGrid - 1) / kFusedMinGrid + 1));
-    size_t o = 0;
-    w.evt = o;     o = align16(o + 4 * (size_t)B);
-    w.stop = o;    o = align16(o + 4 * (size_t)B);
-    w.ticketA = o; o = align16(o + 4 * rows);
-    w.ticketB = o; o = align16(o + 4 * rows);
-    w.glob = o;    o = align16(o + 16);
-    w.mbox_tail = o; o = align16(o + 4 * (size_t)kFusedMaxGrid);
-    w.mbox = o;    o = align16(o + 4 * (size_t)kFusedMaxGrid * w.mcap);
-    w.zero_bytes = o;
-    w.rowstat = o; o = align16(o + sizeof(RowStat) * rows);
-    w.cand = o;    o = align16(o + 8 * rows);
-    w.partA = o;   o = align16(o + sizeof(PartA) * rows * w.nch);
-    w.partB = o;   o = align16(o + sizeof(PartB) * rows * w.nch);
-    w.segtab = o;  o = align16(o + 16 * rows * w.nch * fused::kSegsH);
-    w.total = o;
-    return w;
-}
-
-inline int fused_max_vocab(int32_t esz) { return 255 * (fused::kRowChunkBytesH / esz); }
 
 }  // namespace sd

@@ -214,6 +214,104 @@ __device__ __forceinline__ void thread_stats(const float (&v)[NV][VEC], float c2
     s = x0 + x1;
 }
 
+// The last CTA of a row pair combines its nch slice partials (fp64) and takes the decision
+// (warp 0 of the caller).
+template <bool GREEDY>
+__device__ __forceinline__ void row_decide(const Params& P, int b, int j, int x, int lane) {
+    const int nch = P.nch, kk = P.k;
+    const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
+    const bool load_q = !GREEDY && j < kk;
+    __threadfence();
+    const PartA* parts = P.partA + pos * nch;
+    float RMp = -INFINITY, RMq = -INFINITY, zxp = 0.0f, zxq = 0.0f;
+    int flags = 0, RG = INT_MAX, hasx_lane = 0;
+    for (int cc = lane; cc < nch; cc += 32) {
+        const PartA a = load_cg(parts + cc);
+        flags |= a.flags;
+        if (a.flags & kPartHasX) {
+            zxp = a.zx_p;
+            zxq = a.zx_q;
+            hasx_lane = 1;
+        }
+        if (GREEDY) {
+            if (a.M_p > RMp || (a.M_p == RMp && a.argmax < RG)) {
+                RMp = a.M_p;
+                RG = a.argmax;
+            }
+        } else {
+            RMp = fmaxf(RMp, a.M_p);
+            RMq = fmaxf(RMq, a.M_q);
+        }
+    }
+    if (GREEDY) {
+        warp_argmax(RMp, RG);
+    } else {
+        RMp = warp_max(RMp);
+        RMq = warp_max(RMq);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) flags |= __shfl_xor_sync(0xFFFFFFFFu, flags, o);
+    const unsigned hx = __ballot_sync(0xFFFFFFFFu, hasx_lane);
+    if (hx) {
+        const int src = __ffs(hx) - 1;
+        zxp = __shfl_sync(0xFFFFFFFFu, zxp, src);
+        zxq = __shfl_sync(0xFFFFFFFFu, zxq, src);
+    }
+    double RSp = 0.0, RSq = 0.0;
+    if (!GREEDY) {
+        // rescale each slice sum from its own scaled max to the row's: S_c * 2^(D_c - D)
+        for (int cc = lane; cc < nch; cc += 32) {
+            const PartA a = load_cg(parts + cc);
+            if (a.S_p > 0.0) RSp += a.S_p * exp2(static_cast<double>(a.M_p) - static_cast<double>(RMp));
+            if (a.S_q > 0.0) RSq += a.S_q * exp2(static_cast<double>(a.M_q) - static_cast<double>(RMq));
+        }
+        RSp = warp_sum(RSp);
+        RSq = warp_sum(RSq);
+    }
+    if (lane != 0) return;
+
+    int32_t st = 0;
+    bool stop = false;
+    if (j < kk && (x < 0 || x >= P.V)) st = kBadId;
+    if (!st) {
+        if (flags & kPartNonfiniteP) st = kNonfinite;
+        else if (RMp == -INFINITY) st = kEmptyRow;
+    }
+    if (!st && load_q) {
+        if (flags & kPartNonfiniteQ) st = kNonfinite;
+        else if (RMq == -INFINITY) st = kEmptyRow;
+    }
+    if (st) {
+        stop = true;
+    } else if (j < kk) {
+        if (GREEDY) {
+            stop = (x != RG);                                       // argmax matching (C-5)
+        } else if (zxq == -INFINITY) {
+            st = kZeroQ;                                            // q_j(x_j) = 0 (C-7)
+            stop = true;
+        } else {
+            // a = p(x)/q(x) = 2^((z_p(x) c2 - D_p) - (z_q(x) c2 - D_q)) * S_q / S_p
+            const double l = (static_cast<double>(zxp) * P.c2d - static_cast<double>(RMp)) -
+                             (static_cast<double>(zxq) * P.c2d - static_cast<double>(RMq));
+            const double a = exp2(l) * (RSq / RSp);
+            if (!(a >= 1.0)) {                                      // a = min(1, p/q) < 1
+                const uint4 w = verify_words(P.seed, static_cast<uint32_t>(j), P.round,
+                                             P.rid_base + static_cast<uint64_t>(b));
+                stop = unit24(w.x) >= a;                            // reject iff u >= a (C-2)
+            }
+        }
+    }
+    RowStat rs;
+    rs.S_p = RSp;
+    rs.S_q = RSq;
+    rs.M_p = RMp;
+    rs.M_q = RMq;
+    rs.status = st;
+    rs.argmax = RG;
+    P.rowstat[pos] = rs;
+    if (stop) atomicOr(P.rej_mask + b, 1u << j);
+}
+
 // ------------------------------------------------------------------------------------------
 // Kernel A: per-slice statistics + per-row acceptance decision
 template <typename E, bool GREEDY>
@@ -251,13 +349,10 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
         fence_mbar_init();
     }
     __syncthreads();
-    if (s_flag) {   // the request already stopped before j: this row is never needed
-        if (tid == 0) {
-            const uint32_t t = atomicAdd(P.ticketA + pos, kSkipArrive);
-            if ((t & 0xFFFFu) == static_cast<uint32_t>(nch - 1)) P.ticketA[pos] = 0u;
-        }
-        return;
-    }
+    // The request already stopped before j: this row is never needed (laziness).  No ticket is
+    // taken: a needed row (j <= L) can never see a stop bit below j, so all its chunks arrive;
+    // the request's finalizer resets every ticket of the request for the next call.
+    if (s_flag) return;
 
     const int c0 = c * P.CH;
     const int len = min(P.CH, P.V - c0);
@@ -410,106 +505,15 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
                 pa.flags |= kPartHasX;
             }
             P.partA[pos * nch + c] = pa;
-            __threadfence();
-            const uint32_t t = atomicAdd(P.ticketA + pos, 1u);
-            const bool last = (t & 0xFFFFu) == static_cast<uint32_t>(nch - 1);
-            if (last) P.ticketA[pos] = 0u;
-            s_flag = last && (t >> 16) == 0u;   // last arriver and no slice of this row skipped
+            uint32_t t;   // release: the partial is visible before the ticket
+            asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(P.ticketA + pos) : "memory");
+            s_flag = t == static_cast<uint32_t>(nch - 1);   // last arriver of the row
         }
     }
     __syncthreads();
     if (!s_flag || warp != 0) return;
 
-    // ---- last CTA of the row pair: combine the slices (fp64) and decide --------------------
-    __threadfence();
-    const PartA* parts = P.partA + pos * nch;
-    float RMp = -INFINITY, RMq = -INFINITY, zxp = 0.0f, zxq = 0.0f;
-    int flags = 0, RG = INT_MAX, hasx_lane = 0;
-    for (int cc = lane; cc < nch; cc += 32) {
-        const PartA a = load_cg(parts + cc);
-        flags |= a.flags;
-        if (a.flags & kPartHasX) {
-            zxp = a.zx_p;
-            zxq = a.zx_q;
-            hasx_lane = 1;
-        }
-        if (GREEDY) {
-            if (a.M_p > RMp || (a.M_p == RMp && a.argmax < RG)) {
-                RMp = a.M_p;
-                RG = a.argmax;
-            }
-        } else {
-            RMp = fmaxf(RMp, a.M_p);
-            RMq = fmaxf(RMq, a.M_q);
-        }
-    }
-    if (GREEDY) {
-        warp_argmax(RMp, RG);
-    } else {
-        RMp = warp_max(RMp);
-        RMq = warp_max(RMq);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) flags |= __shfl_xor_sync(0xFFFFFFFFu, flags, o);
-    const unsigned hx = __ballot_sync(0xFFFFFFFFu, hasx_lane);
-    if (hx) {
-        const int src = __ffs(hx) - 1;
-        zxp = __shfl_sync(0xFFFFFFFFu, zxp, src);
-        zxq = __shfl_sync(0xFFFFFFFFu, zxq, src);
-    }
-    double RSp = 0.0, RSq = 0.0;
-    if (!GREEDY) {
-        // rescale each slice sum from its own scaled max to the row's: S_c * 2^(D_c - D)
-        for (int cc = lane; cc < nch; cc += 32) {
-            const PartA a = load_cg(parts + cc);
-            if (a.S_p > 0.0) RSp += a.S_p * exp2(static_cast<double>(a.M_p) - static_cast<double>(RMp));
-            if (a.S_q > 0.0) RSq += a.S_q * exp2(static_cast<double>(a.M_q) - static_cast<double>(RMq));
-        }
-        RSp = warp_sum(RSp);
-        RSq = warp_sum(RSq);
-    }
-    if (lane != 0) return;
-
-    int32_t st = 0;
-    bool stop = false;
-    if (j < kk && (x < 0 || x >= P.V)) st = kBadId;
-    if (!st) {
-        if (flags & kPartNonfiniteP) st = kNonfinite;
-        else if (RMp == -INFINITY) st = kEmptyRow;
-    }
-    if (!st && load_q) {
-        if (flags & kPartNonfiniteQ) st = kNonfinite;
-        else if (RMq == -INFINITY) st = kEmptyRow;
-    }
-    if (st) {
-        stop = true;
-    } else if (j < kk) {
-        if (GREEDY) {
-            stop = (x != RG);                                       // argmax matching (C-5)
-        } else if (zxq == -INFINITY) {
-            st = kZeroQ;                                            // q_j(x_j) = 0 (C-7)
-            stop = true;
-        } else {
-            // a = p(x)/q(x) = 2^((z_p(x) c2 - D_p) - (z_q(x) c2 - D_q)) * S_q / S_p
-            const double l = (static_cast<double>(zxp) * P.c2d - static_cast<double>(RMp)) -
-                             (static_cast<double>(zxq) * P.c2d - static_cast<double>(RMq));
-            const double a = exp2(l) * (RSq / RSp);
-            if (!(a >= 1.0)) {                                      // a = min(1, p/q) < 1
-                const uint4 w = verify_words(P.seed, static_cast<uint32_t>(j), P.round,
-                                             P.rid_base + static_cast<uint64_t>(b));
-                stop = unit24(w.x) >= a;                            // reject iff u >= a (C-2)
-            }
-        }
-    }
-    RowStat rs;
-    rs.S_p = RSp;
-    rs.S_q = RSq;
-    rs.M_p = RMp;
-    rs.M_q = RMq;
-    rs.status = st;
-    rs.argmax = RG;
-    P.rowstat[pos] = rs;
-    if (stop) atomicOr(P.rej_mask + b, 1u << j);
+    row_decide<GREEDY>(P, b, j, x, lane);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -801,6 +805,7 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
         if (P.out_status) P.out_status[b] = status;
         P.rej_mask[b] = 0u;      // leave the workspace zeroed for the next call
         P.ticketB[b] = 0u;
+        for (int i = 0; i <= kk; ++i) P.ticketA[static_cast<size_t>(b) * (kk + 1) + i] = 0u;
     }
 }
 
@@ -824,6 +829,7 @@ __global__ void k_finalize_greedy(const Params P) {
     }
     if (P.out_status) P.out_status[b] = rs.status;
     P.rej_mask[b] = 0u;
+    for (int i = 0; i <= kk; ++i) P.ticketA[static_cast<size_t>(b) * (kk + 1) + i] = 0u;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -867,6 +873,14 @@ void record_event(cudaEvent_t ev, cudaStream_t st) {
     else
         cudaEventRecord(ev, st);
 }
+template <typename E, bool G>
+static void launch_stats(const Params& P, cudaStream_t st) {
+    const int nb = (P.B + kGridY - 1) / kGridY;
+    const dim3 gridA(P.nch, P.B < kGridY ? P.B : kGridY, (P.k + 1) * nb);
+    const size_t sm = (G ? 1 : 2) * static_cast<size_t>(P.CH) * sizeof(E);
+    k_row_stats<E, G><<<gridA, kThreads, sm, st>>>(P);
+}
+
 template <typename E>
 static cudaError_t launch_sampled(const Params& P, cudaStream_t st, cudaEvent_t ev0,
                                   cudaEvent_t ev1) {
@@ -881,9 +895,8 @@ static cudaError_t launch_sampled(const Params& P, cudaStream_t st, cudaEvent_t 
         attr = true;
     }
     const int nb = (P.B + kGridY - 1) / kGridY;
-    const dim3 gridA(P.nch, P.B < kGridY ? P.B : kGridY, (P.k + 1) * nb);
     record_event(ev0, st);
-    k_row_stats<E, false><<<gridA, kThreads, smem, st>>>(P);
+    launch_stats<E, false>(P, st);
     record_event(ev1, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -901,10 +914,8 @@ static cudaError_t launch_greedy(const Params& P, cudaStream_t st, cudaEvent_t e
                              kMaxChunkBytes * 2);
         attr = true;
     }
-    const int nb = (P.B + kGridY - 1) / kGridY;
-    const dim3 gridA(P.nch, P.B < kGridY ? P.B : kGridY, (P.k + 1) * nb);
     record_event(ev0, st);
-    k_row_stats<E, true><<<gridA, kThreads, smem, st>>>(P);
+    launch_stats<E, true>(P, st);
     record_event(ev1, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

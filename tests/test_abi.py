@@ -121,3 +121,17 @@ def test_product_package_never_imports_the_oracle():
             src = open(os.path.join(ROOT, "oracle", f)).read()
             assert "import paper_2601" not in src and "from paper_2601" not in src, f
             assert not re.search(r'#include\s*[<"][^>"]*starsd\.h', src), f
+
+
+def test_verify_plan_default_is_two_launch_with_16kb_chunks(lib):
+    """sd_verify_plan on the host: the default variant, its launch count and chunking (Llama-3
+    shape: V=128256 fp32 -> 32 chunks of 4096 logits = 16 KB, grid (k+1)*B*nch CTAs)."""
+    import torch
+    import paper_2601_21622_b200 as sd
+    pl = sd.plan(128, 7, 128256, 1.0)
+    assert pl["variant"] == "two_launch" and pl["launches"] == 2
+    assert pl["slice"] == 4096 and pl["ctas"] == 8 * 128 * 32
+    plb = sd.plan(64, 5, 32000, 0.0, torch.bfloat16)          # bf16: 8192 logits per 16 KB chunk
+    assert plb["slice"] == 8192 and plb["ctas"] == 6 * 64 * 4
+    with pytest.raises(sd.StarsdError):
+        sd.plan(4, 40, 1000, 1.0)                               # k > 31 rejected on the host

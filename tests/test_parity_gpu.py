@@ -225,3 +225,37 @@ def test_gpu_monte_carlo_matches_exact_outcome():
     keep = exact * B > 5
     g = 2 * np.sum(obs[keep] * np.log(np.maximum(obs[keep], 1) / (B * exact[keep])))
     assert st.chi2.sf(g, keep.sum() - 1) > 1e-4
+
+
+def test_stream_variant_matches_the_oracle():
+    """The opt-in persistent cluster kernel (STARSD_KERNEL=stream) against the oracle on the
+    same cases as the default path (a separate process: the variant is chosen once per process)."""
+    import subprocess
+    import sys
+    code = r'''
+import os, sys
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+import numpy as np, torch
+import paper_2601_21622_b200 as sd
+import oracle
+from parity import compare
+from workload import make_batch
+assert sd.plan(64, 5, 32000, 1.0)["variant"] == "stream"
+for (V, k, B, T, ld) in [(32000, 5, 64, 1.0, 32000), (32000, 5, 64, 0.0, 32000), (1003, 3, 50, 1.0, 1004),
+                         (12345, 6, 9, 0.5, 12348)]:
+    d = make_batch(V=V, k=k, B=B, T=max(T, 1e-3), kappa=10.0, seed=V + k, ld=ld)
+    dev = torch.device("cuda:0")
+    p = torch.from_numpy(d["p"]).to(dev); q = torch.from_numpy(d["q"]).to(dev); ids = torch.from_numpy(d["ids"]).to(dev)
+    L, tok, st = sd.verify(p, q if T > 0 else None, ids, T, seed=1234, round=5, request_id_base=1000, vocab=V)
+    torch.cuda.synchronize()
+    gpu = (L.cpu().numpy(), tok.cpu().numpy(), st.cpu().numpy())
+    ref = oracle.verify(d["p"], d["q"] if T > 0 else None, d["ids"], T, seed=1234, round=5, rid_base=1000,
+                        V=V, trace=True, n_threads=8)
+    stats = compare(d, gpu, ref, T, 1234, 5, 1000, V=V)
+    assert stats["ties"] <= max(1, 2e-2 * stats["n"]), stats
+print("STREAM_OK")
+'''
+    env = dict(os.environ, STARSD_KERNEL="stream")
+    r = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert "STREAM_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
