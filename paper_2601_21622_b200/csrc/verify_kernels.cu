@@ -810,6 +810,264 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
 }
 
 // ------------------------------------------------------------------------------------------
+// Kernel B (one CTA per request): residual (or bonus) inverse-CDF sample at the stop position L.
+//
+// The CTA streams row L of its request -- units of kSUnit logits of p_L and q_L -- through a ring
+// of kSRing shared-memory slots (lane 0 copies p, lane 1 copies q: two issuing threads keep two
+// bulk copies in flight), computes r = max(0, p - q) (or p) per 16-byte vector and one fp64 mass
+// per 32-vector segment (a warp tree reduction), keeps every segment mass of the row in shared
+// memory, and searches blocks of 32 segments -> segment -> lane -> token on chip; only the found
+// segment is re-read (32 vectors).  No ticket, no global segment table.
+constexpr int kSThreadsB = 512;
+constexpr int kSRing = 3;                         // ring slots (p unit | q unit each)
+constexpr int kSUnitBytes = 32 * 1024;            // bytes of p (and of q) per unit: one bulk copy
+                                                  // per issuing thread (tools/tma_probe)
+constexpr int kSMaxSeg = 2048;                    // segments per row kept in shared memory
+                                                  // (V <= 262144 fp32 / 524288 bf16)
+
+template <typename E>
+__global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params P) {
+    using EL = Elt<E>;
+    constexpr int VEC = EL::VEC;
+    constexpr int NT = kSThreadsB, NW = NT / 32;   // consumer warps; warp NW is the producer
+    constexpr int SEGV = 32;                                  // vectors per segment
+    constexpr int UV = kSUnitBytes / 16;                      // vectors per unit
+    constexpr int USEG = UV / SEGV;                           // segments per unit
+    extern __shared__ __align__(128) unsigned char smem[];    // ring, then segment masses
+    double* segm = reinterpret_cast<double*>(smem + static_cast<size_t>(kSRing) * 2 * kSUnitBytes);
+    __shared__ __align__(8) uint64_t full[kSRing][2], empty[kSRing];
+    __shared__ double s_blk[kSMaxSeg / 32];                   // block (32-segment) masses
+    __shared__ double s_th;
+    __shared__ int s_sel[2];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int kk = P.k;
+    const int b = blockIdx.x;
+    if (tid == 0) {
+        for (int i = 0; i < kSRing; ++i) {
+            mbar_init(&full[i][0], 1);
+            mbar_init(&full[i][1], 1);
+            mbar_init(&empty[i], NW);
+        }
+        fence_mbar_init();
+    }
+    // programmatic dependent launch: wait until every decision of k_row_stats is visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint32_t mask = P.rej_mask[b];
+    const int L = mask ? __ffs(mask) - 1 : kk;
+    const RowStat rs = load_cg(P.rowstat + static_cast<size_t>(b) * (kk + 1) + L);
+    const bool hard = (rs.status & kHard) != 0;
+    const bool use_q = L < kk;
+    const float c2 = P.c2;
+    const E* gp = static_cast<const E*>(P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
+    const E* gq = use_q ? static_cast<const E*>(P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q
+                        : nullptr;
+    const int V = P.V;
+    const int nvv = (V + VEC - 1) / VEC;                      // vectors of the row
+    const int nunits = (nvv + UV - 1) / UV;
+    const int nseg = (nvv + SEGV - 1) / SEGV;
+    const uint32_t rowbytes = static_cast<uint32_t>(nvv) * 16u;   // staged bytes (16 B rounded)
+    __syncthreads();
+    int32_t status = rs.status;
+    int32_t tok = -1;
+    if (!hard) {
+        ResidParams rp;
+        rp.nDp = -rs.M_p;
+        rp.nDq = use_q ? -rs.M_q : 0.0f;
+        rp.ip = static_cast<float>(1.0 / rs.S_p);
+        rp.iq = use_q ? static_cast<float>(1.0 / rs.S_q) : 0.0f;
+        rp.use_q = use_q ? 1 : 0;
+        bool zero_res = false;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            // ---- stream the row: unit u in slot u % kSRing --------------------------------
+            auto issue = [&](int u) {
+                const int sl = u % kSRing;
+                const uint32_t off = static_cast<uint32_t>(u) * kSUnitBytes;
+                const uint32_t nb = min(static_cast<uint32_t>(kSUnitBytes), rowbytes - off);
+                unsigned char* dst = smem + static_cast<size_t>(sl) * 2 * kSUnitBytes;
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&full[sl][0], nb);
+                    bulk_g2s(dst, reinterpret_cast<const char*>(gp) + off, nb, &full[sl][0]);
+                } else if (lane == 1 && rp.use_q) {
+                    mbar_arrive_expect_tx(&full[sl][1], nb);
+                    bulk_g2s(dst + kSUnitBytes, reinterpret_cast<const char*>(gq) + off, nb, &full[sl][1]);
+                }
+            };
+            const int base_u = attempt * nunits;               // ring position of unit 0
+            if (warp == NW) {
+                // producer warp: lane 0 streams p, lane 1 streams q, each as far ahead as the ring allows
+                for (int u = 0; u < nunits; ++u) {
+                    const int n = base_u + u;
+                    if (n >= kSRing) mbar_wait(&empty[n % kSRing], ((n / kSRing) & 1) ^ 1);
+                    issue(n);
+                }
+            } else {
+                for (int u = 0; u < nunits; ++u) {
+                    const int n = base_u + u, sl = n % kSRing;
+                    const uint32_t ph = (n / kSRing) & 1;
+                    mbar_wait(&full[sl][0], ph);
+                    if (rp.use_q) mbar_wait(&full[sl][1], ph);
+                    const uint4* sp4 = reinterpret_cast<const uint4*>(smem + static_cast<size_t>(sl) * 2 * kSUnitBytes);
+                    const uint4* sq4 = sp4 + UV;
+                    for (int sg = warp; sg < USEG; sg += NW) {
+                        const int g = u * UV + sg * SEGV + lane;    // row vector index
+                        const int valid = min(VEC, max(0, V - g * VEC));
+                        uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
+                        if (g < nvv) {
+                            up = sp4[sg * SEGV + lane];
+                            if (rp.use_q) uq = sq4[sg * SEGV + lane];
+                        }
+                        float r[VEC], pv[VEC], sr, spv;
+                        resid_terms<E>(up, uq, valid, rp, c2, r, pv, sr, spv);
+                        const double m = warp_sum(static_cast<double>(rp.use_q ? sr : spv));
+                        const int gs = u * USEG + sg;
+                        if (lane == 0 && gs < nseg) segm[gs] = m;
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[sl]);
+                }
+            }
+            __syncthreads();
+            // ---- block masses (32 segments each; warp tree sums) and the total --------------
+            const int nblk = (nseg + 31) / 32;
+            for (int bk = warp; bk < nblk; bk += NW) {
+                const int sgi = bk * 32 + lane;
+                const double t = warp_sum(sgi < nseg ? segm[sgi] : 0.0);
+                if (lane == 0) s_blk[bk] = t;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                // level 1: blocks (<= NW * 4 of them) -- warp scans with a carry
+                const uint4 w = verify_words(P.seed, static_cast<uint32_t>(L), P.round,
+                                             P.rid_base + static_cast<uint64_t>(b));
+                double carry = 0.0;
+                for (int base = 0; base < nblk; base += 32) {
+                    double v = base + lane < nblk ? s_blk[base + lane] : 0.0;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
+                        if (lane >= o) v = __dadd_rn(v, a);
+                    }
+                    carry = __dadd_rn(carry, __shfl_sync(0xFFFFFFFFu, v, 31));
+                }
+                const double tot = carry;
+                if (lane == 0) s_sel[1] = tot > 0.0;
+                if (tot > 0.0) {
+                    const double theta = unit24(w.y) * tot;      // C-9: first x with C(x) > theta
+                    int bsel = -1, blast = 0;
+                    double run = 0.0, th = INFINITY;
+                    for (int base = 0; base < nblk && bsel < 0; base += 32) {
+                        const double m = base + lane < nblk ? s_blk[base + lane] : 0.0;
+                        double v = m;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
+                            if (lane >= o) v = __dadd_rn(v, a);
+                        }
+                        v = __dadd_rn(run, v);
+                        const unsigned h = __ballot_sync(0xFFFFFFFFu, base + lane < nblk && v > theta);
+                        const unsigned pm = __ballot_sync(0xFFFFFFFFu, base + lane < nblk && m > 0.0);
+                        if (pm) blast = base + 31 - __clz(pm);
+                        if (h) {
+                            const int l = __ffs(h) - 1;
+                            double e = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+                            if (lane == 0) e = run;
+                            bsel = base + l;
+                            th = theta - __shfl_sync(0xFFFFFFFFu, e, l);
+                        }
+                        run = __shfl_sync(0xFFFFFFFFu, v, 31);
+                    }
+                    if (bsel < 0) bsel = blast;                  // rounding: last block with mass
+                    // level 2: the block's 32 segments
+                    const int sgi = bsel * 32 + lane;
+                    const double m = sgi < nseg ? segm[sgi] : 0.0;
+                    double v = m;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
+                        if (lane >= o) v = __dadd_rn(v, a);
+                    }
+                    const unsigned h = __ballot_sync(0xFFFFFFFFu, sgi < nseg && v > th);
+                    const unsigned pm = __ballot_sync(0xFFFFFFFFu, sgi < nseg && m > 0.0);
+                    const int ls = h ? __ffs(h) - 1 : (pm ? 31 - __clz(pm) : 0);
+                    double e = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+                    if (lane == 0) e = 0.0;
+                    const double th2 = h ? th - __shfl_sync(0xFFFFFFFFu, e, ls) : INFINITY;
+                    if (lane == 0) {
+                        s_sel[0] = bsel * 32 + ls;
+                        s_th = th2;
+                    }
+                }
+            }
+            __syncthreads();
+            if (s_sel[1] || !rp.use_q) {
+                zero_res = attempt == 1;
+                break;
+            }
+            // C-6: the residual has no mass (rounding only): sample from p_L instead
+            rp.use_q = 0;
+            __syncthreads();
+        }
+        // ---- level 3: re-read the found segment, scan it, find the lane and the token -------
+        if (warp == 0) {
+            const int sgsel = s_sel[0];
+            const double th2 = s_th;
+            const int g = sgsel * SEGV + lane;
+            const int valid = min(VEC, max(0, V - g * VEC));
+            uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
+            if (g < nvv) {
+                up = __ldcg(reinterpret_cast<const uint4*>(gp) + g);
+                if (rp.use_q) uq = __ldcg(reinterpret_cast<const uint4*>(gq) + g);
+            }
+            float r[VEC], pv[VEC], sr, spv;
+            resid_terms<E>(up, uq, valid, rp, c2, r, pv, sr, spv);
+            double v = static_cast<double>(rp.use_q ? sr : spv);
+            const float mine = rp.use_q ? sr : spv;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
+                if (lane >= o) v = __dadd_rn(v, a);
+            }
+            const unsigned hit = __ballot_sync(0xFFFFFFFFu, v > th2);
+            const unsigned posm = __ballot_sync(0xFFFFFFFFu, mine > 0.0f);
+            const int ls = hit ? __ffs(hit) - 1 : (posm ? 31 - __clz(posm) : 0);
+            double ex = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+            if (lane == 0) ex = 0.0;
+            int fe = -1;
+            if (lane == ls) {
+                const double th3 = hit ? th2 - ex : INFINITY;
+                int lastpos = -1;
+                float cum = 0.0f;
+#pragma unroll
+                for (int e2 = 0; e2 < VEC; ++e2) {
+                    const float te = rp.use_q ? r[e2] : pv[e2];
+                    if (te > 0.0f) lastpos = e2;
+                    cum = e2 == 0 ? te : __fadd_rn(cum, te);
+                    if (fe < 0 && static_cast<double>(cum) > th3) fe = e2;
+                }
+                if (fe < 0) fe = lastpos >= 0 ? lastpos : 0;   // rounding: clamp (C-9)
+            }
+            fe = __shfl_sync(0xFFFFFFFFu, fe, ls);
+            tok = (sgsel * SEGV + ls) * VEC + fe;
+            if (zero_res) status |= kZeroResidual;
+        }
+    }
+    if (tid == 0) {
+        const int Lout = hard ? 0 : L;
+        P.out_L[b] = Lout;
+        int32_t* ot = P.out_tok + static_cast<size_t>(b) * (kk + 1);
+        for (int i = 0; i <= kk; ++i) {
+            int32_t v = -1;
+            if (!hard) v = i < L ? P.ids[static_cast<size_t>(b) * kk + i] : (i == L ? tok : -1);
+            ot[i] = v;
+        }
+        if (P.out_status) P.out_status[b] = status;
+        P.rej_mask[b] = 0u;      // leave the workspace zeroed for the next call
+        for (int i = 0; i <= kk; ++i) P.ticketA[static_cast<size_t>(b) * (kk + 1) + i] = 0u;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // Greedy finalize: one thread per request
 __global__ void k_finalize_greedy(const Params P) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -900,6 +1158,16 @@ static cudaError_t launch_sampled(const Params& P, cudaStream_t st, cudaEvent_t 
     record_event(ev1, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    const int nseg_row = (P.V + 32 * (16 / static_cast<int>(sizeof(E))) - 1) / (32 * (16 / static_cast<int>(sizeof(E))));
+    if (nseg_row <= kSMaxSeg) {
+        static bool attr2 = false;
+        const size_t smB = static_cast<size_t>(kSRing) * 2 * kSUnitBytes + sizeof(double) * kSMaxSeg;
+        if (!attr2) {
+            cudaFuncSetAttribute(k_sample_req<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smB));
+            attr2 = true;
+        }
+        return launch_dependent(k_sample_req<E>, dim3(P.B), kSThreadsB + 32, smB, st, P);
+    }
     return launch_dependent(k_sample<E>, dim3(P.nch, P.B < kGridY ? P.B : kGridY, nb), kThreads, smem,
                             st, P);
 }
