@@ -885,10 +885,12 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
                 const uint32_t off = static_cast<uint32_t>(u) * kSUnitBytes;
                 const uint32_t nb = min(static_cast<uint32_t>(kSUnitBytes), rowbytes - off);
                 unsigned char* dst = smem + static_cast<size_t>(sl) * 2 * kSUnitBytes;
-                if (lane == 0) {
+                // a different lane pair per slot: a thread's bulk copies complete one after
+                // another, so rotating issuers keeps every slot's copies in flight together
+                if (lane == 2 * sl) {
                     mbar_arrive_expect_tx(&full[sl][0], nb);
                     bulk_g2s(dst, reinterpret_cast<const char*>(gp) + off, nb, &full[sl][0]);
-                } else if (lane == 1 && rp.use_q) {
+                } else if (lane == 2 * sl + 1 && rp.use_q) {
                     mbar_arrive_expect_tx(&full[sl][1], nb);
                     bulk_g2s(dst + kSUnitBytes, reinterpret_cast<const char*>(gq) + off, nb, &full[sl][1]);
                 }
@@ -909,20 +911,34 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
                     if (rp.use_q) mbar_wait(&full[sl][1], ph);
                     const uint4* sp4 = reinterpret_cast<const uint4*>(smem + static_cast<size_t>(sl) * 2 * kSUnitBytes);
                     const uint4* sq4 = sp4 + UV;
-                    for (int sg = warp; sg < USEG; sg += NW) {
+                    // warp w: segments 4w .. 4w+3 of the unit (one vector per lane each), then one
+                    // transpose-reduce of the four fp64 masses (12 shuffles instead of 40)
+                    static_assert(USEG == 4 * NW, "four segments per consumer warp and unit");
+                    double d[4];
+#pragma unroll
+                    for (int k4 = 0; k4 < 4; ++k4) {
+                        const int sg = 4 * warp + k4;
                         const int g = u * UV + sg * SEGV + lane;    // row vector index
-                        const int valid = min(VEC, max(0, V - g * VEC));
                         uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
                         if (g < nvv) {
                             up = sp4[sg * SEGV + lane];
                             if (rp.use_q) uq = sq4[sg * SEGV + lane];
                         }
+                        const int valid = g < nvv - 1 ? VEC : min(VEC, max(0, V - g * VEC));
                         float r[VEC], pv[VEC], sr, spv;
                         resid_terms<E>(up, uq, valid, rp, c2, r, pv, sr, spv);
-                        const double m = warp_sum(static_cast<double>(rp.use_q ? sr : spv));
-                        const int gs = u * USEG + sg;
-                        if (lane == 0 && gs < nseg) segm[gs] = m;
+                        d[k4] = static_cast<double>(rp.use_q ? sr : spv);
                     }
+                    const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
+                    double a0 = b4 ? d[2] : d[0], a1 = b4 ? d[3] : d[1];
+                    a0 = __dadd_rn(a0, __shfl_xor_sync(0xFFFFFFFFu, b4 ? d[0] : d[2], 16));
+                    a1 = __dadd_rn(a1, __shfl_xor_sync(0xFFFFFFFFu, b4 ? d[1] : d[3], 16));
+                    double m = b3 ? a1 : a0;
+                    m = __dadd_rn(m, __shfl_xor_sync(0xFFFFFFFFu, b3 ? a0 : a1, 8));
+#pragma unroll
+                    for (int o = 4; o > 0; o >>= 1) m = __dadd_rn(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+                    const int gs = u * USEG + 4 * warp + 2 * b4 + b3;   // this lane group's segment
+                    if ((lane & 7) == 0 && gs < nseg) segm[gs] = m;
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[sl]);
                 }

@@ -259,3 +259,12 @@ print("STREAM_OK")
     r = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                        env=env, capture_output=True, text=True, timeout=600)
     assert "STREAM_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("T", [1.0, 0.0])
+def test_parity_vocab_beyond_the_on_chip_sampler(T):
+    """V = 300000 (fp32) exceeds the per-request sampler's on-chip segment table (2048 segments
+    of 128 logits): the chunked sampling kernel serves it; both must match the oracle."""
+    V = 300000
+    d = make_batch(V=V, k=2, B=6, T=max(T, 1e-3), kappa=10.0, seed=300000, ld=V)
+    check(d, T, V=V, max_tie_frac=2e-1)
