@@ -572,6 +572,43 @@ __device__ __forceinline__ void resid_terms(uint4 up, uint4 uq, int valid, const
         spv = __fadd_rn(spv, pv[u]);
     }
 }
+// Scaled residual terms for the per-request sampler: with e_p = 2^(z_p c2 - D_p) and
+// e_q = 2^(z_q c2 - D_q), r(x) * S_p = max(0, e_p - rho * e_q), rho = S_p / S_q, or e_p
+// (bonus row / zero-residual fallback, rho < 0 means "no q").  The common factor 1/S_p cancels
+// in the inverse CDF, so the sampler works with these scaled terms throughout.  Past-the-end
+// lanes (>= valid) are 0.  Returns the sequential fp32 sum (the order the search re-uses).
+template <typename E>
+__device__ __forceinline__ float resid_scaled(uint4 up, uint4 uq, int valid, float c2, float nDp,
+                                              float nDq, float rho, float (&r)[Elt<E>::VEC]) {
+    using EL = Elt<E>;
+    constexpr int VEC = EL::VEC;
+    float v[VEC];
+    EL::unpack(up, v);
+    const unsigned long long cc = pk2(c2, c2), np = pk2(nDp, nDp);
+#pragma unroll
+    for (int u = 0; u < VEC; u += 2) upk2(ex2x2(ffma2(pk2(v[u], v[u + 1]), cc, np)), r[u], r[u + 1]);
+    if (rho >= 0.0f) {
+        float w[VEC];
+        EL::unpack(uq, w);
+        const unsigned long long nq = pk2(nDq, nDq), nr = pk2(-rho, -rho);
+#pragma unroll
+        for (int u = 0; u < VEC; u += 2) {
+            float t0, t1;
+            upk2(ffma2(ex2x2(ffma2(pk2(w[u], w[u + 1]), cc, nq)), nr, pk2(r[u], r[u + 1])), t0, t1);
+            r[u] = fmaxf(t0, 0.0f);
+            r[u + 1] = fmaxf(t1, 0.0f);
+        }
+    }
+    if (valid < VEC) {
+#pragma unroll
+        for (int u = 0; u < VEC; ++u)
+            if (u >= valid) r[u] = 0.0f;
+    }
+    float sr = r[0];
+#pragma unroll
+    for (int u = 1; u < VEC; ++u) sr = __fadd_rn(sr, r[u]);
+    return sr;
+}
 // inclusive Kogge-Stone scan of (R, P) pairs over the lanes (fixed association)
 __device__ __forceinline__ double2 warp_scan2(double2 v, int lane) {
 #pragma unroll
@@ -877,6 +914,7 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
         rp.ip = static_cast<float>(1.0 / rs.S_p);
         rp.iq = use_q ? static_cast<float>(1.0 / rs.S_q) : 0.0f;
         rp.use_q = use_q ? 1 : 0;
+        float rho = use_q ? static_cast<float>(rs.S_p / rs.S_q) : -1.0f;   // < 0: p only
         bool zero_res = false;
         for (int attempt = 0; attempt < 2; ++attempt) {
             // ---- stream the row: unit u in slot u % kSRing --------------------------------
@@ -925,9 +963,8 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
                             if (rp.use_q) uq = sq4[sg * SEGV + lane];
                         }
                         const int valid = g < nvv - 1 ? VEC : min(VEC, max(0, V - g * VEC));
-                        float r[VEC], pv[VEC], sr, spv;
-                        resid_terms<E>(up, uq, valid, rp, c2, r, pv, sr, spv);
-                        d[k4] = static_cast<double>(rp.use_q ? sr : spv);
+                        float r[VEC];
+                        d[k4] = static_cast<double>(resid_scaled<E>(up, uq, valid, c2, rp.nDp, rp.nDq, rho, r));
                     }
                     const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
                     double a0 = b4 ? d[2] : d[0], a1 = b4 ? d[3] : d[1];
@@ -1022,6 +1059,7 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
             }
             // C-6: the residual has no mass (rounding only): sample from p_L instead
             rp.use_q = 0;
+            rho = -1.0f;
             __syncthreads();
         }
         // ---- level 3: re-read the found segment, scan it, find the lane and the token -------
@@ -1035,10 +1073,10 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
                 up = __ldcg(reinterpret_cast<const uint4*>(gp) + g);
                 if (rp.use_q) uq = __ldcg(reinterpret_cast<const uint4*>(gq) + g);
             }
-            float r[VEC], pv[VEC], sr, spv;
-            resid_terms<E>(up, uq, valid, rp, c2, r, pv, sr, spv);
-            double v = static_cast<double>(rp.use_q ? sr : spv);
-            const float mine = rp.use_q ? sr : spv;
+            float r[VEC];
+            const float sr = resid_scaled<E>(up, uq, g < nvv - 1 ? VEC : valid, c2, rp.nDp, rp.nDq, rho, r);
+            double v = static_cast<double>(sr);
+            const float mine = sr;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
@@ -1056,7 +1094,7 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
                 float cum = 0.0f;
 #pragma unroll
                 for (int e2 = 0; e2 < VEC; ++e2) {
-                    const float te = rp.use_q ? r[e2] : pv[e2];
+                    const float te = r[e2];
                     if (te > 0.0f) lastpos = e2;
                     cum = e2 == 0 ? te : __fadd_rn(cum, te);
                     if (fe < 0 && static_cast<double>(cum) > th3) fe = e2;
