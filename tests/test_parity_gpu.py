@@ -268,3 +268,33 @@ def test_parity_vocab_beyond_the_on_chip_sampler(T):
     V = 300000
     d = make_batch(V=V, k=2, B=6, T=max(T, 1e-3), kappa=10.0, seed=300000, ld=V)
     check(d, T, V=V, max_tie_frac=2e-1)
+
+
+@pytest.mark.parametrize("T", [1.0, 0.0])
+def test_parity_max_chain_length(T):
+    """k = 31 (the ballot/mask limit): 32 positions per request at the Vicuna vocabulary."""
+    d = make_batch(V=32000, k=31, B=8, T=max(T, 1e-3), kappa=300.0, seed=3131)
+    check(d, T)
+
+
+def test_parity_single_request_llama3_vocab():
+    """B = 1 at V = 128256: one request's rows spread over the whole grid / one sampler CTA."""
+    d = make_batch(V=128256, k=7, B=1, T=1.0, kappa=30.0, seed=128)
+    check(d, 1.0)
+    check(d, 0.0)
+
+
+def test_parity_bf16_ragged_vocab_and_padding():
+    """bf16 with a vocabulary that is not a multiple of the 8-logit vector, NaN-padded rows."""
+    V = 12345
+    d = make_batch(V=V, k=4, B=24, T=1.0, kappa=30.0, seed=12345, dtype="bf16", ld=12352)
+    gpu, ref, _ = check(d, 1.0, V=V, max_tie_frac=2e-2)
+    assert np.all(gpu[2] == 0)
+    check(d, 0.0, V=V)
+
+
+@pytest.mark.parametrize("T", [0.05, 5.0])
+def test_parity_extreme_temperatures(T):
+    """Very peaked (T = 0.05: c2 = log2(e)/T ~ 29) and very flat (T = 5) distributions."""
+    d = make_batch(V=32000, k=5, B=32, T=T, kappa=30.0, seed=int(T * 1000) + 7)
+    check(d, T, max_tie_frac=2e-2)
