@@ -198,6 +198,9 @@ typedef struct {
                             all world-1 verifiers on one device; the exchange is a D2D copy on
                             the pair's stream and the draft's round desc carries p_logits.
                             Same scheduler, poll and stats code as the NCCL transport.       */
+    float target_ms;     /* verifier-side stand-in for the target model's forward (t_v of Eq.
+                            6): a device-side spin of this many ms on the verifier's
+                            stream before each verify (0 = none); used by tools/star_bench.py  */
 } sd_star_config;
 
 enum { SD_STAR_NCCL = 0, SD_STAR_LOOPBACK = 1 };

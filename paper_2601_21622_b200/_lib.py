@@ -43,7 +43,7 @@ class StarConfig(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("n_slots", ctypes.c_int32),
                 ("max_shape", Shape), ("temperature", ctypes.c_float), ("seed", ctypes.c_uint64),
                 ("timeout_ms", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("transport", ctypes.c_int32)]
+                ("transport", ctypes.c_int32), ("target_ms", ctypes.c_float)]
 
 
 SD_STAR_NCCL, SD_STAR_LOOPBACK = 0, 1

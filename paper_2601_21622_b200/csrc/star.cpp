@@ -27,6 +27,7 @@
 #endif
 
 namespace sd {
+cudaError_t launch_spin_ns(uint64_t ns, cudaStream_t st);   // verify_kernels.cu
 
 // ---- the scheduler: transport-agnostic, host-only ---------------------------------------
 struct Ret {
@@ -330,6 +331,7 @@ sd_status sd_star_round(sd_star* h, const sd_round_desc* d, cudaStream_t stream)
             if (!greedy)
                 SD_CUDA(cudaMemcpyAsync(h->q_buf[i], d->q_logits, B * k * V * h->esz,
                                         cudaMemcpyDeviceToDevice, cs));
+            if (h->cfg.target_ms > 0.0f) SD_CUDA(launch_spin_ns(static_cast<uint64_t>(h->cfg.target_ms * 1e6), cs));
             sd_shape sh = ms;
             sh.batch = d->batch;
             sd_status st = sd_verify(d->p_logits, greedy ? nullptr : h->q_buf[i], h->ids_buf[i], &sh,
@@ -365,6 +367,7 @@ sd_status sd_star_round(sd_star* h, const sd_round_desc* d, cudaStream_t stream)
     SD_NCCL(ncclRecv(ids, B * k, ncclInt32, 0, h->comms[0], stream));
     if (!greedy) SD_NCCL(ncclRecv(q, B * k * V, dt, 0, h->comms[0], stream));
     SD_NCCL(ncclGroupEnd());
+    if (h->cfg.target_ms > 0.0f) SD_CUDA(launch_spin_ns(static_cast<uint64_t>(h->cfg.target_ms * 1e6), stream));
     sd_shape sh = ms;
     sh.batch = d->batch;
     sd_status st = sd_verify(d->p_logits, greedy ? nullptr : q, ids, &sh, h->cfg.temperature,

@@ -1253,6 +1253,21 @@ cudaError_t launch_verify(const Params& P, bool greedy, bool bf16, cudaStream_t 
                 : launch_sampled<float>(P, st, ev0, ev1);
 }
 
+// Device-side stand-in for a model forward of a given duration (star benchmarks): one thread
+// spins on %globaltimer.
+__global__ void k_spin_ns(uint64_t ns) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        __nanosleep(1000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+cudaError_t launch_spin_ns(uint64_t ns, cudaStream_t st) {
+    k_spin_ns<<<1, 32, 0, st>>>(ns);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_philox(uint64_t seed, uint64_t round, const uint32_t* pos, const uint64_t* rid,
                           int n, uint32_t* out, cudaStream_t st) {
     if (n > 0) k_philox<<<(n + 255) / 256, 256, 0, st>>>(seed, round, pos, rid, n, out);

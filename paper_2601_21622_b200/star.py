@@ -82,7 +82,7 @@ class Star:
     def __init__(self, rank: int, world: int, max_batch: int, k: int, vocab: int,
                  temperature: float, seed: int = 0, n_slots: int = 2,
                  dtype: torch.dtype = torch.float32, device=None, ids: bytes | None = None,
-                 transport: str = "nccl", timeout_ms: int = 60000):
+                 transport: str = "nccl", timeout_ms: int = 60000, target_ms: float = 0.0):
         dev = torch.device(device if device is not None else "cuda")
         if dev.type != "cuda":
             raise StarsdError("Star needs a CUDA device")
@@ -95,7 +95,7 @@ class Star:
                               _lib.Shape(max_batch, k, vocab, vocab, vocab, _dt(dtype)),
                               self.temperature, seed, timeout_ms,
                               dev.index if dev.index is not None else torch.cuda.current_device(),
-                              tcode)
+                              tcode, float(target_ms))
         self._h = ctypes.c_void_p()
         idbuf = None if ids is None else ctypes.create_string_buffer(ids, len(ids))
         check(self._L.sd_star_create(ctypes.byref(self._h), ctypes.byref(cfg), idbuf),

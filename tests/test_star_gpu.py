@@ -83,3 +83,20 @@ def test_loopback_rejects_misuse():
     with pytest.raises(star.StarsdError, match="INVALID_ARGUMENT"):
         h.draft_end()                                   # end without begin
     h.close()
+
+
+@pytest.mark.parametrize("N", [1, 2, 5])
+def test_loopback_busy_fraction_follows_sec41_closed_form(N):
+    """Draft service S and target stand-in Z as device spins (tools/star_bench.py): the measured
+    draft busy fraction follows Eqs. 7-10 -- Z/S = 3 gives N_full = 4."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "star_bench", os.path.join(os.path.dirname(__file__), "..", "tools", "star_bench.py"))
+    sb = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(sb)
+    S, Z = 1.0, 3.0
+    st = sb.run(N, 1, S, Z, 20, sb.sleep_cycles_per_ms(), 8, 4, 4096)
+    pred = star.predicted(N, S, Z)
+    assert st["rounds"] == 20 * N
+    assert abs(st["busy_fraction"] - pred["busy_fraction"]) < 0.08, (st, pred)
