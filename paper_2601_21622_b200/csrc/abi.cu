@@ -191,6 +191,8 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     P.ld_p = shape->ld_p ? shape->ld_p : shape->vocab;
     P.ld_q = shape->ld_q ? shape->ld_q : shape->vocab;
     chunking(P.V, esz, &P.nch, &P.CH);
+    P.CL = row_cluster(P.nch);
+    P.G = (P.nch + P.CL - 1) / P.CL;
     P.nseg = P.CH / (32 * (kVecBytes / esz));
     P.c2 = c2;
     P.c2d = static_cast<double>(P.c2);
@@ -198,6 +200,7 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     P.round = round;
     P.rid_base = request_id_base;
     P.out_L = out_accept_len;
+    P.trace = g_trace;
     P.out_tok = out_tokens;
     P.out_status = out_status;
     P.rej_mask = reinterpret_cast<uint32_t*>(ws + w.rej_mask);
@@ -237,7 +240,9 @@ sd_status sd_verify_plan(const sd_shape* shape, float temperature, sd_plan* out)
     out->variant = SD_VARIANT_TWO_LAUNCH;
     out->launches = 2;
     out->slice = CH;
-    out->ctas = (int64_t)(shape->k + 1) * shape->batch * nch;
+    const int32_t CL = row_cluster(nch), G = (nch + CL - 1) / CL;
+    out->cluster = CL > 1 ? CL : 0;
+    out->ctas = (int64_t)(shape->k + 1) * shape->batch * (CL > 1 ? G * CL : nch);
     return SD_OK;
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <vector_types.h>
 
 namespace sd {
@@ -11,7 +12,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kVecBytes = 16;            // one 128-bit smem/global vector per thread per tile
 constexpr int kTileBytes = kThreads * kVecBytes;   // 4 KB of one row per tile
 constexpr int kMaxChunkBytes = 16 * 1024;          // one CTA owns <= 16 KB of a row (measured best of 8/16/32 KB)
-                                                   // (one 32 KB bulk copy per row and CTA)
+constexpr int kRowClusterDefault = 8;              // see row_cluster()
 
 // Per (request b, position j, vocab chunk c): what one kernel-A CTA found in its slice.
 struct PartA {
@@ -21,7 +22,7 @@ struct PartA {
     int32_t flags;       // kPartNonfiniteP | kPartNonfiniteQ | kPartHasX
     int32_t argmax;      // greedy: lowest index of the slice max (global token id)
 };
-constexpr int32_t kPartNonfiniteP = 1, kPartNonfiniteQ = 2, kPartHasX = 4;
+constexpr int32_t kPartNonfiniteP = 1, kPartNonfiniteQ = 2, kPartHasX = 4, kPartSkipped = 8;
 
 // Per (request b, position j): the whole-row statistics, written by the last kernel-A CTA of
 // that row pair, read by the sampling kernel.
@@ -45,6 +46,9 @@ struct Params {
     int32_t B, k, V;
     int64_t ld_p, ld_q;          // elements
     int32_t nch;                 // vocab chunks per row
+    int32_t CL;                  // k_row_stats cluster size (1: no cluster; chunk partials of a
+                                 // cluster meet in its rank-0 CTA's shared memory)
+    int32_t G;                   // row partials published to partA per row: ceil(nch / CL)
     int32_t CH;                  // elements per chunk (multiple of the tile)
     float c2;                    // log2(e) / T   (fp32; sampled path)
     double c2d;                  // the same value widened (exactly) to fp64
@@ -61,7 +65,31 @@ struct Params {
     PartB* partB;                // [B][nch]
     double2* segtab;             // [B][nch][nseg]  (r mass, p mass) per warp segment
     int32_t nseg;                // segments per chunk
+    unsigned long long* trace;   // debug builds only (SD_STREAM_DEBUG): per-CTA phase timestamps
 };
+
+// k_row_stats cluster size for a row of nch chunks: a cluster covers the whole row when nch <= 8
+// (the smallest power of two >= nch; the grid's x extent is padded with empty chunks), so the
+// row's partials meet in the leader's shared memory and no global ticket is taken.  Longer rows
+// (nch > 8) measured faster without clusters (profiles/README.md).  STARSD_ROWCLUSTER=n caps the
+// size (1 = the cluster-free kernel); a negative value -n forces clusters of n on every row
+// (G = ceil(nch / n) cluster partials per row then meet through a global ticket).
+inline int32_t row_cluster(int32_t nch) {
+    static int env = 0;
+    static bool read = false;
+    if (!read) {
+        const char* e = getenv("STARSD_ROWCLUSTER");
+        env = e ? atoi(e) : 0;
+        read = true;
+    }
+    if (env < 0) {
+        const int f = -env;
+        return (f == 2 || f == 4 || f == 8) ? (nch > 1 ? f : 1) : 1;
+    }
+    const int cap = (env == 1 || env == 2 || env == 4 || env == 8) ? env : kRowClusterDefault;
+    const int32_t c = nch > 8 ? 1 : nch > 4 ? 8 : nch > 2 ? 4 : nch > 1 ? 2 : 1;
+    return c < cap ? c : cap;
+}
 
 // Workspace layout for a shape; all offsets 16-byte aligned.  The first `zero_bytes` must be
 // zero before a call and are zero again after it.

@@ -37,7 +37,6 @@ namespace sd {
 constexpr int32_t kBadId = 1, kNonfinite = 2, kEmptyRow = 4, kZeroQ = 8, kZeroResidual = 16;
 constexpr int32_t kHard = kBadId | kNonfinite | kEmptyRow;
 constexpr int kGridY = 32768;   // requests per grid.y span (gridDim.y <= 65535)
-constexpr uint32_t kSkipArrive = 1u | (1u << 16);
 
 // ------------------------------------------------------------------------------------------
 // element types: one 16-byte vector holds 4 fp32 or 8 bf16 logits
@@ -214,19 +213,21 @@ __device__ __forceinline__ void thread_stats(const float (&v)[NV][VEC], float c2
     s = x0 + x1;
 }
 
-// The last CTA of a row pair combines its nch slice partials (fp64) and takes the decision
-// (warp 0 of the caller).
-template <bool GREEDY>
-__device__ __forceinline__ void row_decide(const Params& P, int b, int j, int x, int lane) {
-    const int nch = P.nch, kk = P.k;
-    const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
-    const bool load_q = !GREEDY && j < kk;
-    __threadfence();
-    const PartA* parts = P.partA + pos * nch;
+// Combination of n slice partials (fp64, exact 2^(D_c - D) rescales); warp-collective, the
+// result is valid in every lane.  SHARED: the partials sit in this CTA's shared memory (cluster
+// leader), else in global memory written by other CTAs of this launch.
+struct Comb {
+    float RMp, RMq, zxp, zxq;
+    double RSp, RSq;
+    int flags, RG;
+};
+
+template <bool GREEDY, bool SHARED>
+__device__ __forceinline__ Comb combine_parts(const PartA* parts, int n, int lane) {
     float RMp = -INFINITY, RMq = -INFINITY, zxp = 0.0f, zxq = 0.0f;
     int flags = 0, RG = INT_MAX, hasx_lane = 0;
-    for (int cc = lane; cc < nch; cc += 32) {
-        const PartA a = load_cg(parts + cc);
+    for (int cc = lane; cc < n; cc += 32) {
+        const PartA a = SHARED ? parts[cc] : load_cg(parts + cc);
         flags |= a.flags;
         if (a.flags & kPartHasX) {
             zxp = a.zx_p;
@@ -260,40 +261,70 @@ __device__ __forceinline__ void row_decide(const Params& P, int b, int j, int x,
     double RSp = 0.0, RSq = 0.0;
     if (!GREEDY) {
         // rescale each slice sum from its own scaled max to the row's: S_c * 2^(D_c - D)
-        for (int cc = lane; cc < nch; cc += 32) {
-            const PartA a = load_cg(parts + cc);
+        for (int cc = lane; cc < n; cc += 32) {
+            const PartA a = SHARED ? parts[cc] : load_cg(parts + cc);
             if (a.S_p > 0.0) RSp += a.S_p * exp2(static_cast<double>(a.M_p) - static_cast<double>(RMp));
             if (a.S_q > 0.0) RSq += a.S_q * exp2(static_cast<double>(a.M_q) - static_cast<double>(RMq));
         }
         RSp = warp_sum(RSp);
         RSq = warp_sum(RSq);
     }
-    if (lane != 0) return;
+    Comb C;
+    C.RMp = RMp;
+    C.RMq = RMq;
+    C.zxp = zxp;
+    C.zxq = zxq;
+    C.RSp = RSp;
+    C.RSq = RSq;
+    C.flags = flags;
+    C.RG = RG;
+    return C;
+}
 
+// The combined statistics of a group of slices, as one partial of the next level.
+__device__ __forceinline__ PartA comb_as_part(const Comb& C) {
+    PartA a;
+    a.S_p = C.RSp;
+    a.S_q = C.RSq;
+    a.M_p = C.RMp;
+    a.M_q = C.RMq;
+    a.zx_p = C.zxp;
+    a.zx_q = C.zxq;
+    a.flags = C.flags;
+    a.argmax = C.RG;
+    return a;
+}
+
+// The acceptance decision of row pair (b, j) from its whole-row statistics (one thread).
+template <bool GREEDY>
+__device__ __forceinline__ void decide(const Params& P, int b, int j, int x, const Comb& C) {
+    const int kk = P.k;
+    const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
+    const bool load_q = !GREEDY && j < kk;
     int32_t st = 0;
     bool stop = false;
     if (j < kk && (x < 0 || x >= P.V)) st = kBadId;
     if (!st) {
-        if (flags & kPartNonfiniteP) st = kNonfinite;
-        else if (RMp == -INFINITY) st = kEmptyRow;
+        if (C.flags & kPartNonfiniteP) st = kNonfinite;
+        else if (C.RMp == -INFINITY) st = kEmptyRow;
     }
     if (!st && load_q) {
-        if (flags & kPartNonfiniteQ) st = kNonfinite;
-        else if (RMq == -INFINITY) st = kEmptyRow;
+        if (C.flags & kPartNonfiniteQ) st = kNonfinite;
+        else if (C.RMq == -INFINITY) st = kEmptyRow;
     }
     if (st) {
         stop = true;
     } else if (j < kk) {
         if (GREEDY) {
-            stop = (x != RG);                                       // argmax matching (C-5)
-        } else if (zxq == -INFINITY) {
+            stop = (x != C.RG);                                     // argmax matching (C-5)
+        } else if (C.zxq == -INFINITY) {
             st = kZeroQ;                                            // q_j(x_j) = 0 (C-7)
             stop = true;
         } else {
             // a = p(x)/q(x) = 2^((z_p(x) c2 - D_p) - (z_q(x) c2 - D_q)) * S_q / S_p
-            const double l = (static_cast<double>(zxp) * P.c2d - static_cast<double>(RMp)) -
-                             (static_cast<double>(zxq) * P.c2d - static_cast<double>(RMq));
-            const double a = exp2(l) * (RSq / RSp);
+            const double l = (static_cast<double>(C.zxp) * P.c2d - static_cast<double>(C.RMp)) -
+                             (static_cast<double>(C.zxq) * P.c2d - static_cast<double>(C.RMq));
+            const double a = exp2(l) * (C.RSq / C.RSp);
             if (!(a >= 1.0)) {                                      // a = min(1, p/q) < 1
                 const uint4 w = verify_words(P.seed, static_cast<uint32_t>(j), P.round,
                                              P.rid_base + static_cast<uint64_t>(b));
@@ -302,25 +333,141 @@ __device__ __forceinline__ void row_decide(const Params& P, int b, int j, int x,
         }
     }
     RowStat rs;
-    rs.S_p = RSp;
-    rs.S_q = RSq;
-    rs.M_p = RMp;
-    rs.M_q = RMq;
+    rs.S_p = C.RSp;
+    rs.S_q = C.RSq;
+    rs.M_p = C.RMp;
+    rs.M_q = C.RMq;
     rs.status = st;
-    rs.argmax = RG;
+    rs.argmax = C.RG;
     P.rowstat[pos] = rs;
     if (stop) atomicOr(P.rej_mask + b, 1u << j);
 }
 
+// The last publisher of a row pair combines the row's G published partials (fp64) and takes the
+// decision (warp 0 of the caller).
+template <bool GREEDY>
+__device__ __forceinline__ void row_decide(const Params& P, int b, int j, int x, int lane) {
+    const size_t pos = static_cast<size_t>(b) * (P.k + 1) + j;
+    __threadfence();
+    const Comb C = combine_parts<GREEDY, false>(P.partA + pos * P.nch, P.G, lane);
+    if (lane == 0) decide<GREEDY>(P, b, j, x, C);
+}
+
+// Development timeline (debug builds, sd_debug_trace): slot i of the CTA's 8-word record gets
+// %globaltimer; word 7 = smid << 32 | flags (1 skipped, 2 last arriver, 4 stop).
+#if SD_STREAM_DEBUG
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SD_TR(P, i)                                                                          \
+    do {                                                                                     \
+        if ((P).trace)                                                                       \
+            (P).trace[((static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + \
+                       blockIdx.x) * 8 + (i)] = gtimer();                                    \
+    } while (0)
+#define SD_TRF(P, f)                                                                         \
+    do {                                                                                     \
+        if ((P).trace) {                                                                     \
+            uint32_t smid;                                                                   \
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));                                \
+            (P).trace[((static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + \
+                       blockIdx.x) * 8 + 7] = (static_cast<unsigned long long>(smid) << 32) | (f); \
+        }                                                                                    \
+    } while (0)
+// k_sample_req: records after k_row_stats' grid, one per request
+#define SD_TRS(P, i)                                                                         \
+    do {                                                                                     \
+        if ((P).trace) {                                                                     \
+            const size_t nbq = ((P).B + kGridY - 1) / kGridY;                                \
+            const size_t gA = static_cast<size_t>((P).nch) * ((P).B < kGridY ? (P).B : kGridY) * \
+                              ((P).k + 1) * nbq;                                             \
+            (P).trace[(gA + blockIdx.x) * 8 + (i)] = gtimer();                               \
+        }                                                                                    \
+    } while (0)
+#else
+#define SD_TR(P, i) do {} while (0)
+#define SD_TRF(P, f) do {} while (0)
+#define SD_TRS(P, i) do {} while (0)
+#endif
+
+// ---- cluster publish (k_row_stats with CL > 1) --------------------------------------------
+// A peer's partial goes into the leader's slot with five asynchronous 8-byte stores that complete
+// transaction bytes on the leader's s_pbar (armed for (CL-1) * 40 bytes): no release fence.
+__device__ __forceinline__ void cl_send_part(uint32_t raddr, const PartA& a, uint32_t rbar) {
+    static_assert(sizeof(PartA) == 40, "PartA is five 8-byte words");
+    const uint2* w = reinterpret_cast<const uint2*>(&a);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) cl_st_async_v2(raddr + 8 * i, w[i], rbar);
+}
+
+// Warp 0 of a CTA of cluster g of row pair (b, j); `pa` is valid in lane 0.
+template <bool GREEDY, int CL>
+__device__ __forceinline__ void cluster_publish(const Params& P, const PartA& pa, PartA* s_parts,
+                                                uint64_t* s_pbar, int rank, int g, int b, int j,
+                                                int x, int lane) {
+    if (rank != 0) {
+        if (lane == 0) {
+            cl_wait_acquire();                       // the leader's s_pbar is initialised
+            cl_send_part(cl_map(&s_parts[rank], 0), pa, cl_map(s_pbar, 0));
+            SD_TR(P, 5);
+            SD_TR(P, 6);
+            SD_TRF(P, 0);
+        }
+        return;
+    }
+    if (lane == 0) s_parts[0] = pa;
+    while (!mbar_try_wait_cluster(s_pbar, 0)) {
+    }
+    __syncwarp();
+    const Comb C = combine_parts<GREEDY, true>(s_parts, CL, lane);
+    if (C.flags & kPartSkipped) return;   // a peer saw a stop below j: the row is not needed
+    if (P.G == 1) {                       // the cluster covers the row: decide at once
+        if (lane == 0) {
+            SD_TR(P, 5);
+            decide<GREEDY>(P, b, j, x, C);
+            SD_TR(P, 6);
+            SD_TRF(P, 2);
+        }
+        return;
+    }
+    const size_t pos = static_cast<size_t>(b) * (P.k + 1) + j;
+    uint32_t t = 0;
+    if (lane == 0) {
+        P.partA[pos * P.nch + g] = comb_as_part(C);
+        // release: the partial is visible before the ticket
+        asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(P.ticketA + pos) : "memory");
+        SD_TR(P, 5);
+    }
+    t = __shfl_sync(0xFFFFFFFFu, t, 0);
+    if (t != static_cast<uint32_t>(P.G - 1)) {
+        if (lane == 0) { SD_TR(P, 6); SD_TRF(P, 0); }
+        return;
+    }
+    row_decide<GREEDY>(P, b, j, x, lane);
+    if (lane == 0) { SD_TR(P, 6); SD_TRF(P, 2); }
+}
+
 // ------------------------------------------------------------------------------------------
 // Kernel A: per-slice statistics + per-row acceptance decision
-template <typename E, bool GREEDY>
-__global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
+//
+// CL > 1: the grid's x extent is G * CL (chunks padded with empty ones) in clusters of CL along
+// x.  A non-leader CTA sends its partial into the leader's (rank 0) shared memory with st.async
+// stores that complete bytes on the leader's mbarrier, then exits: no fence, no global atomic on
+// its path.  The leader
+// combines the CL partials; with G == 1 it decides at once, else it publishes the cluster partial
+// and takes the row ticket (the last of the G leaders decides).  Every CTA of a cluster arrives
+// exactly once, also when it skips, so the leader outlives every remote write into it.
+template <typename E, bool GREEDY, int CL>
+__global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
     using EL = Elt<E>;
     constexpr int VEC = EL::VEC;
     constexpr int NV = kMaxChunkBytes / kVecBytes / kThreads;   // 16-byte vectors per thread
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
+    __shared__ __align__(8) uint64_t s_pbar;                    // CL > 1, leader: peer partials
+    __shared__ __align__(16) PartA s_parts[CL];
     __shared__ int s_flag;
     __shared__ float s_d[2][kWarps];
     __shared__ double s_s[2][kWarps];
@@ -341,21 +488,46 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
     }
     const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
 
+    const int rank = CL > 1 ? c % CL : 0;
     if (tid == 0) {
+        SD_TR(P, 0);
         const uint32_t m = j ? ld_relaxed_u32(P.rej_mask + b) : 0u;
         s_flag = (m & ((1u << j) - 1u)) != 0u;
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
+        if (CL > 1 && rank == 0) mbar_init(&s_pbar, 1);
         fence_mbar_init();
+        if (CL > 1 && rank == 0) mbar_arrive_expect_tx(&s_pbar, (CL - 1) * sizeof(PartA));
     }
     __syncthreads();
+    // the leader's barrier is initialised before any peer writes into it: every thread arrives on
+    // the cluster barrier now, the one thread that writes into the leader waits on it late
+    if (CL > 1) cl_arrive_relaxed();
     // The request already stopped before j: this row is never needed (laziness).  No ticket is
     // taken: a needed row (j <= L) can never see a stop bit below j, so all its chunks arrive;
     // the request's finalizer resets every ticket of the request for the next call.
-    if (s_flag) return;
+    if (s_flag) {
+        if (tid == 0) {
+            SD_TR(P, 1);
+            SD_TRF(P, 1);
+            if (CL > 1) {
+                if (rank != 0) {
+                    cl_wait_acquire();
+                    PartA a{};
+                    a.flags = kPartSkipped;
+                    cl_send_part(cl_map(&s_parts[rank], 0), a, cl_map(&s_pbar, 0));
+                } else {
+                    while (!mbar_try_wait_cluster(&s_pbar, 0)) {
+                    }
+                }
+            }
+        }
+        return;
+    }
+    if (tid == 0) SD_TR(P, 1);
 
     const int c0 = c * P.CH;
-    const int len = min(P.CH, P.V - c0);
+    const int len = max(0, min(P.CH, P.V - c0));   // CL > 1: empty padding chunks past V
     const bool load_q = !GREEDY && j < kk;
     const E* gp = static_cast<const E*>(P.p) + static_cast<int64_t>(pos) * P.ld_p + c0;
     const E* gq = load_q ? static_cast<const E*>(P.q) +
@@ -386,6 +558,7 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
     const int nvv = (len + VEC - 1) / VEC;       // vectors incl. a ragged last one
     float vp[NV][VEC];
     mbar_wait(&bar[0], 0);
+    if (tid == 0) SD_TR(P, 2);
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         const int g = tid + i * kThreads;
@@ -430,6 +603,7 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
         if (load_q) {
             float vq[NV][VEC];
             mbar_wait(&bar[1], 0);
+            if (tid == 0) SD_TR(P, 3);
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
                 const int g = tid + i * kThreads;
@@ -473,6 +647,8 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
         }
     }
     __syncthreads();
+    if (tid == 0) SD_TR(P, 4);
+    if (CL > 1 && warp != 0) return;
     if (warp == 0) {
         const bool on = lane < kWarps;
         const int f = __reduce_or_sync(0xFFFFFFFFu, on ? s_f[lane] : 0);
@@ -504,16 +680,27 @@ __global__ void __launch_bounds__(kThreads) k_row_stats(const Params P) {
                 pa.zx_q = load_q ? EL::one(sq, x - c0) : 0.0f;
                 pa.flags |= kPartHasX;
             }
+        }
+        if (CL > 1) {
+            cluster_publish<GREEDY, CL>(P, pa, s_parts, &s_pbar, rank, c / CL, b, j, x, lane);
+            return;
+        }
+        if (lane == 0) {
             P.partA[pos * nch + c] = pa;
             uint32_t t;   // release: the partial is visible before the ticket
             asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(P.ticketA + pos) : "memory");
             s_flag = t == static_cast<uint32_t>(nch - 1);   // last arriver of the row
+            SD_TR(P, 5);
         }
     }
     __syncthreads();
-    if (!s_flag || warp != 0) return;
+    if (!s_flag || warp != 0) {
+        if (tid == 0) { SD_TR(P, 6); SD_TRF(P, 0); }
+        return;
+    }
 
     row_decide<GREEDY>(P, b, j, x, lane);
+    if (tid == 0) { SD_TR(P, 6); SD_TRF(P, 2); }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -888,8 +1075,10 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
         }
         fence_mbar_init();
     }
+    if (tid == 0) SD_TRS(P, 0);
     // programmatic dependent launch: wait until every decision of k_row_stats is visible
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid == 0) SD_TRS(P, 1);
     const uint32_t mask = P.rej_mask[b];
     const int L = mask ? __ffs(mask) - 1 : kk;
     const RowStat rs = load_cg(P.rowstat + static_cast<size_t>(b) * (kk + 1) + L);
@@ -1118,6 +1307,7 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
         if (P.out_status) P.out_status[b] = status;
         P.rej_mask[b] = 0u;      // leave the workspace zeroed for the next call
         for (int i = 0; i <= kk; ++i) P.ticketA[static_cast<size_t>(b) * (kk + 1) + i] = 0u;
+        SD_TRS(P, 2);
     }
 }
 
@@ -1185,12 +1375,37 @@ void record_event(cudaEvent_t ev, cudaStream_t st) {
     else
         cudaEventRecord(ev, st);
 }
+template <typename E, bool G, int CL>
+static void launch_stats_cl(const Params& P, cudaStream_t st) {
+    const int nb = (P.B + kGridY - 1) / kGridY;
+    const dim3 gridA(CL > 1 ? P.G * CL : P.nch, P.B < kGridY ? P.B : kGridY, (P.k + 1) * nb);
+    const size_t sm = (G ? 1 : 2) * static_cast<size_t>(P.CH) * sizeof(E);
+    if (CL == 1) {
+        k_row_stats<E, G, CL><<<gridA, kThreads, sm, st>>>(P);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = gridA;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_row_stats<E, G, CL>, P);
+}
 template <typename E, bool G>
 static void launch_stats(const Params& P, cudaStream_t st) {
-    const int nb = (P.B + kGridY - 1) / kGridY;
-    const dim3 gridA(P.nch, P.B < kGridY ? P.B : kGridY, (P.k + 1) * nb);
-    const size_t sm = (G ? 1 : 2) * static_cast<size_t>(P.CH) * sizeof(E);
-    k_row_stats<E, G><<<gridA, kThreads, sm, st>>>(P);
+    switch (P.CL) {
+        case 8: launch_stats_cl<E, G, 8>(P, st); break;
+        case 4: launch_stats_cl<E, G, 4>(P, st); break;
+        case 2: launch_stats_cl<E, G, 2>(P, st); break;
+        default: launch_stats_cl<E, G, 1>(P, st); break;
+    }
 }
 
 template <typename E>
@@ -1199,7 +1414,7 @@ static cudaError_t launch_sampled(const Params& P, cudaStream_t st, cudaEvent_t 
     const size_t smem = 2 * static_cast<size_t>(P.CH) * sizeof(E);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_row_stats<E, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_row_stats<E, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kMaxChunkBytes * 2);
         cudaFuncSetAttribute(k_sample<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kMaxChunkBytes * 2);
@@ -1232,7 +1447,7 @@ static cudaError_t launch_greedy(const Params& P, cudaStream_t st, cudaEvent_t e
     const size_t smem = static_cast<size_t>(P.CH) * sizeof(E);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_row_stats<E, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_row_stats<E, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kMaxChunkBytes * 2);
         attr = true;
     }

@@ -131,7 +131,13 @@ def test_verify_plan_default_is_two_launch_with_16kb_chunks(lib):
     pl = sd.plan(128, 7, 128256, 1.0)
     assert pl["variant"] == "two_launch" and pl["launches"] == 2
     assert pl["slice"] == 4096 and pl["ctas"] == 8 * 128 * 32
+    assert pl["cluster"] == 0                                  # nch = 32 > 8: cluster-free rows
     plb = sd.plan(64, 5, 32000, 0.0, torch.bfloat16)          # bf16: 8192 logits per 16 KB chunk
-    assert plb["slice"] == 8192 and plb["ctas"] == 6 * 64 * 4
+    assert plb["slice"] == 8192 and plb["ctas"] == 6 * 64 * 4 and plb["cluster"] == 4
+    # a cluster covers a whole row of nch <= 8 chunks (power of two, padded with empty chunks)
+    assert sd.plan(64, 5, 32000, 1.0)["cluster"] == 8          # nch = 8
+    p5 = sd.plan(16, 3, 20000, 1.0)                            # nch = 5 -> 8 (3 empty chunks)
+    assert p5["cluster"] == 8 and p5["ctas"] == 4 * 16 * 8
+    assert sd.plan(16, 3, 3000, 1.0)["cluster"] == 0           # one chunk per row
     with pytest.raises(sd.StarsdError):
         sd.plan(4, 40, 1000, 1.0)                               # k > 31 rejected on the host

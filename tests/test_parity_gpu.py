@@ -227,22 +227,35 @@ def test_gpu_monte_carlo_matches_exact_outcome():
     assert st.chi2.sf(g, keep.sum() - 1) > 1e-4
 
 
-def test_stream_variant_matches_the_oracle():
-    """The opt-in persistent cluster kernel (STARSD_KERNEL=stream) against the oracle on the
-    same cases as the default path (a separate process: the variant is chosen once per process)."""
+@pytest.mark.parametrize("env,want", [
+    ({"STARSD_KERNEL": "stream"}, ("stream", None)),
+    ({"STARSD_ROWCLUSTER": "1"}, ("two_launch", 0)),        # cluster-free k_row_stats
+    ({"STARSD_ROWCLUSTER": "-8"}, ("two_launch", 8)),       # clusters of 8 on every row (G > 1)
+    ({"STARSD_ROWCLUSTER": "-2"}, ("two_launch", 2)),
+])
+def test_kernel_variants_match_the_oracle(env, want):
+    """Kernel variants chosen by environment (once per process, so in a subprocess) against the
+    oracle on the default path's cases plus a Llama-3-vocabulary case: the opt-in persistent
+    stream kernel, the cluster-free k_row_stats, and forced clusters whose row partials meet
+    through the global ticket (G = ceil(nch / CL) > 1)."""
+    import json
     import subprocess
     import sys
     code = r'''
-import os, sys
+import os, sys, json
 sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
 import numpy as np, torch
 import paper_2601_21622_b200 as sd
 import oracle
 from parity import compare
 from workload import make_batch
-assert sd.plan(64, 5, 32000, 1.0)["variant"] == "stream"
+want = json.loads(sys.argv[1])
+pl = sd.plan(128, 7, 128256, 1.0)
+assert pl["variant"] == want[0], pl
+if want[1] is not None:
+    assert pl["cluster"] == want[1], pl
 for (V, k, B, T, ld) in [(32000, 5, 64, 1.0, 32000), (32000, 5, 64, 0.0, 32000), (1003, 3, 50, 1.0, 1004),
-                         (12345, 6, 9, 0.5, 12348)]:
+                         (12345, 6, 9, 0.5, 12348), (128256, 3, 6, 1.0, 128256), (128256, 3, 6, 0.0, 128256)]:
     d = make_batch(V=V, k=k, B=B, T=max(T, 1e-3), kappa=10.0, seed=V + k, ld=ld)
     dev = torch.device("cuda:0")
     p = torch.from_numpy(d["p"]).to(dev); q = torch.from_numpy(d["q"]).to(dev); ids = torch.from_numpy(d["ids"]).to(dev)
@@ -253,12 +266,12 @@ for (V, k, B, T, ld) in [(32000, 5, 64, 1.0, 32000), (32000, 5, 64, 0.0, 32000),
                         V=V, trace=True, n_threads=8)
     stats = compare(d, gpu, ref, T, 1234, 5, 1000, V=V)
     assert stats["ties"] <= max(1, 2e-2 * stats["n"]), stats
-print("STREAM_OK")
+print("VARIANT_OK")
 '''
-    env = dict(os.environ, STARSD_KERNEL="stream")
-    r = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert "STREAM_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+    r = subprocess.run([sys.executable, "-c", code, json.dumps(list(want))],
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
+    assert "VARIANT_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
 
 
 @pytest.mark.parametrize("T", [1.0, 0.0])
