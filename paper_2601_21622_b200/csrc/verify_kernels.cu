@@ -26,10 +26,27 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 
 #include "philox.cuh"
 #include "ptx.cuh"
 #include "verify.cuh"
+
+// Spin-wait.  Debug builds (SD_STREAM_DEBUG) bound it and report the site, so a protocol bug
+// shows up as a message instead of a hung GPU.
+#if SD_STREAM_DEBUG
+#define SD_SPIN(cond, code)                                                                     \
+    for (unsigned long long sd_spin_n = 0; !(cond);)                                            \
+        if (++sd_spin_n == (1ull << 24)) {                                                      \
+            printf("SD_SPIN site %d block (%d,%d,%d) thread %d\n", (code), blockIdx.x, blockIdx.y, \
+                   blockIdx.z, threadIdx.x);                                                    \
+            break;                                                                              \
+        }
+#else
+#define SD_SPIN(cond, code) \
+    while (!(cond)) {       \
+    }
+#endif
 
 namespace sd {
 
@@ -211,6 +228,21 @@ __device__ __forceinline__ void thread_stats(const float (&v)[NV][VEC], float c2
     float x0, x1;
     upk2(t, x0, x1);
     s = x0 + x1;
+}
+
+// ---- outputs --------------------------------------------------------------------------------
+// out_accept_len / out_tokens / out_status of request b (one thread)
+__device__ __forceinline__ void write_outputs(const Params& P, int b, int L, int32_t tok,
+                                              int32_t status, bool hard) {
+    const int kk = P.k;
+    P.out_L[b] = hard ? 0 : L;
+    int32_t* ot = P.out_tok + static_cast<size_t>(b) * (kk + 1);
+    for (int i = 0; i <= kk; ++i) {
+        int32_t v = -1;
+        if (!hard) v = i < L ? P.ids[static_cast<size_t>(b) * kk + i] : (i == L ? tok : -1);
+        ot[i] = v;
+    }
+    if (P.out_status) P.out_status[b] = status;
 }
 
 // Combination of n slice partials (fp64, exact 2^(D_c - D) rescales); warp-collective, the
@@ -409,7 +441,6 @@ __device__ __forceinline__ void cluster_publish(const Params& P, const PartA& pa
                                                 int x, int lane) {
     if (rank != 0) {
         if (lane == 0) {
-            cl_wait_acquire();                       // the leader's s_pbar is initialised
             cl_send_part(cl_map(&s_parts[rank], 0), pa, cl_map(s_pbar, 0));
             SD_TR(P, 5);
             SD_TR(P, 6);
@@ -418,8 +449,7 @@ __device__ __forceinline__ void cluster_publish(const Params& P, const PartA& pa
         return;
     }
     if (lane == 0) s_parts[0] = pa;
-    while (!mbar_try_wait_cluster(s_pbar, 0)) {
-    }
+    SD_SPIN(mbar_try_wait_cluster(s_pbar, 0), 1);
     __syncwarp();
     const Comb C = combine_parts<GREEDY, true>(s_parts, CL, lane);
     if (C.flags & kPartSkipped) return;   // a peer saw a stop below j: the row is not needed
@@ -501,24 +531,26 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
     }
     __syncthreads();
     // the leader's barrier is initialised before any peer writes into it: every thread arrives on
-    // the cluster barrier now, the one thread that writes into the leader waits on it late
+    // the cluster barrier now and waits on it before the first remote write (a skipping CTA at
+    // once, a working one after issuing its copies, so the wait overlaps the load).  Every thread
+    // takes part in both halves: a thread parked on a CTA barrier while its peers wait on the
+    // cluster barrier was measured to hang it.
     if (CL > 1) cl_arrive_relaxed();
     // The request already stopped before j: this row is never needed (laziness).  No ticket is
     // taken: a needed row (j <= L) can never see a stop bit below j, so all its chunks arrive;
     // the request's finalizer resets every ticket of the request for the next call.
     if (s_flag) {
+        if (CL > 1) cl_wait_acquire();
         if (tid == 0) {
             SD_TR(P, 1);
             SD_TRF(P, 1);
             if (CL > 1) {
                 if (rank != 0) {
-                    cl_wait_acquire();
                     PartA a{};
                     a.flags = kPartSkipped;
                     cl_send_part(cl_map(&s_parts[rank], 0), a, cl_map(&s_pbar, 0));
                 } else {
-                    while (!mbar_try_wait_cluster(&s_pbar, 0)) {
-                    }
+                    SD_SPIN(mbar_try_wait_cluster(&s_pbar, 0), 2);
                 }
             }
         }
@@ -551,13 +583,14 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
         if (load_q) sq[i] = gq[i];
     }
     const int x = (j < kk) ? P.ids[static_cast<size_t>(b) * kk + j] : -1;
+    if (CL > 1) cl_wait_acquire();   // (copies in flight) the leader's s_pbar is initialised
     __syncthreads();
 
     // ---- registers: NV vectors of p (and q) per thread; -inf past the slice end ------------
     const int nfull = len / VEC;                 // complete vectors
     const int nvv = (len + VEC - 1) / VEC;       // vectors incl. a ragged last one
     float vp[NV][VEC];
-    mbar_wait(&bar[0], 0);
+    SD_SPIN(mbar_try_wait(&bar[0], 0), 3);
     if (tid == 0) SD_TR(P, 2);
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -602,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
         thread_stats<NV, VEC>(vp, P.c2, kPartNonfiniteP, dP, sP, nf);
         if (load_q) {
             float vq[NV][VEC];
-            mbar_wait(&bar[1], 0);
+            SD_SPIN(mbar_try_wait(&bar[1], 0), 4);
             if (tid == 0) SD_TR(P, 3);
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
@@ -810,37 +843,21 @@ __device__ __forceinline__ double2 warp_scan2(double2 v, int lane) {
     return v;
 }
 
-// grid (chunk c, request b).  CTA (c, b) stages chunk c of (p_L, q_L) (HBM; L2 when recent),
-// computes r and p per 32-vector segment (warp scans, fp64 segment masses) and the chunk's
-// masses (sequential over its segments).  The last CTA of request b searches chunk -> segment
-// -> token, recomputing the one segment with the identical routine.
+// One chunk of request b's sampling row pair (p_L, q_L) (whole CTA): stage chunk c (HBM; L2
+// when recent), compute r and p per 32-vector segment (warp scans, fp64 segment masses) and the
+// chunk's masses (a warp scan over segment pairs: the search's association), publish them and
+// take the request's ticket.  Returns (in every thread) whether this CTA is the request's last.
+// The mbarrier parities ph0 (p) / ph1 (q) advance with each use.
 template <typename E>
-__global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
+__device__ __forceinline__ bool sample_chunk(const Params& P, unsigned char* smem, uint64_t* bar,
+                                             uint32_t& ph0, uint32_t& ph1, double2* s_seg,
+                                             int* s_last, int b, int L, int c, const RowStat& rs,
+                                             bool hard) {
     using EL = Elt<E>;
     constexpr int VEC = EL::VEC;
-    constexpr int SEGV = 32;                          // vectors per segment (one per lane)
-    constexpr int MAXSEG = kMaxChunkBytes / 16 / SEGV;
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ double2 s_seg[MAXSEG];
-    __shared__ int s_last;
-
+    constexpr int SEGV = 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nch = P.nch, kk = P.k;
-    const int c = blockIdx.x, b = blockIdx.y + blockIdx.z * kGridY;
-    if (b >= P.B) return;   // (whole CTA: the request's tickets count only real CTAs)
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-    }
-    // programmatic dependent launch: this grid may start while k_row_stats drains; wait until
-    // every row decision of the primary grid is complete and visible
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint32_t mask = P.rej_mask[b];
-    const int L = mask ? __ffs(mask) - 1 : kk;
-    const RowStat rs = P.rowstat[static_cast<size_t>(b) * (kk + 1) + L];
-    const bool hard = (rs.status & kHard) != 0;
     const bool use_q = L < kk;
     const float c2 = P.c2;
     ResidParams rp;
@@ -856,8 +873,6 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
     const int len = min(P.CH, P.V - c0);
     const int nvv = (len + VEC - 1) / VEC;            // vectors incl. a ragged last one
     const int nsg = (nvv + SEGV - 1) / SEGV;          // segments in this chunk
-    __syncthreads();
-
     if (!hard) {
         E* sp = reinterpret_cast<E*>(smem);
         E* sq = sp + P.CH;
@@ -875,8 +890,12 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
             if (use_q) sq[i] = gq[c0 + i];
         }
         __syncthreads();
-        mbar_wait(&bar[0], 0);
-        if (use_q) mbar_wait(&bar[1], 0);
+        SD_SPIN(mbar_try_wait(&bar[0], ph0), 5);
+        ph0 ^= 1u;
+        if (use_q) {
+            SD_SPIN(mbar_try_wait(&bar[1], ph1), 6);
+            ph1 ^= 1u;
+        }
         for (int sg = warp; sg < nsg; sg += kWarps) {
             const int g = sg * SEGV + lane;
             const int valid = min(VEC, max(0, len - g * VEC));
@@ -904,129 +923,172 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
     __syncthreads();
     if (tid == 0) {
         const uint32_t t = atomicAdd(P.ticketB + b, 1u);
-        s_last = t == static_cast<uint32_t>(nch - 1);
+        *s_last = t == static_cast<uint32_t>(nch - 1);
     }
     __syncthreads();
-    if (!s_last || warp != 0) return;
+    return *s_last != 0;
+}
 
-    // ---- last CTA of request b: inverse CDF, chunk -> segment -> token ------------------
+// The inverse CDF of request b over its published chunk and segment masses, chunk -> segment ->
+// token (warp 0 of the request's last chunk CTA; the result is valid in every lane).  The one
+// found segment is recomputed with the identical routine, so the search sees exactly the masses
+// the main pass produced; clamps implement C-9, a zero residual falls back to p_L (C-6).
+template <typename E>
+__device__ __forceinline__ int32_t sample_search(const Params& P, int b, int L, const RowStat& rs,
+                                                 int32_t& status, int lane) {
+    using EL = Elt<E>;
+    constexpr int VEC = EL::VEC;
+    constexpr int SEGV = 32;
+    const int nch = P.nch, kk = P.k;
+    const bool use_q = L < kk;
+    const float c2 = P.c2;
+    ResidParams rp;
+    rp.nDp = -rs.M_p;
+    rp.nDq = use_q ? -rs.M_q : 0.0f;
+    rp.ip = static_cast<float>(1.0 / rs.S_p);
+    rp.iq = use_q ? static_cast<float>(1.0 / rs.S_q) : 0.0f;
+    rp.use_q = use_q ? 1 : 0;
+    const E* gp = static_cast<const E*>(P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
+    const E* gq = use_q ? static_cast<const E*>(P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q
+                        : nullptr;
     __threadfence();
-    int32_t status = rs.status;
-    int32_t tok = -1;
-    if (!hard) {
-        // level 1: chunks, one lane each, warp scans over blocks of 32 chunks (carry between blocks)
-        auto chunk_mass = [&](int cc) -> double2 {
-            if (cc >= nch) return make_double2(0.0, 0.0);
-            const PartB t = load_cg(P.partB + static_cast<size_t>(b) * nch + cc);
-            return make_double2(t.R, t.P);
-        };
-        double2 carry = make_double2(0.0, 0.0);
-        for (int base = 0; base < nch; base += 32) {
-            const double2 icb = warp_scan2(chunk_mass(base + lane), lane);
-            carry.x = __dadd_rn(carry.x, __shfl_sync(0xFFFFFFFFu, icb.x, 31));
-            carry.y = __dadd_rn(carry.y, __shfl_sync(0xFFFFFFFFu, icb.y, 31));
-        }
-        const bool zero_res = use_q && !(carry.x > 0.0);        // C-6: fall back to p_L
-        const double tot = zero_res ? carry.y : carry.x;
-        const uint4 w = verify_words(P.seed, static_cast<uint32_t>(L), P.round,
-                                     P.rid_base + static_cast<uint64_t>(b));
-        const double theta = unit24(w.y) * tot;                 // C-9: first x with C(x) > theta
-        int cstar = -1, clast = 0;
-        double th1 = INFINITY, run = 0.0;
-        for (int base = 0; base < nch && cstar < 0; base += 32) {
-            const double2 pb = chunk_mass(base + lane);
-            const double2 icb = warp_scan2(pb, lane);
-            const double icm = __dadd_rn(run, zero_res ? icb.y : icb.x);
-            const double mcm = zero_res ? pb.y : pb.x;
-            const unsigned h = __ballot_sync(0xFFFFFFFFu, base + lane < nch && icm > theta);
-            const unsigned pm = __ballot_sync(0xFFFFFFFFu, base + lane < nch && mcm > 0.0);
-            if (pm) clast = base + 31 - __clz(pm);
-            if (h) {
-                const int l = __ffs(h) - 1;
-                double e = __shfl_up_sync(0xFFFFFFFFu, icm, 1);
-                if (lane == 0) e = run;
-                cstar = base + l;
-                th1 = theta - __shfl_sync(0xFFFFFFFFu, e, l);
-            }
-            run = __shfl_sync(0xFFFFFFFFu, icm, 31);
-        }
-        if (cstar < 0) cstar = clast;                           // rounding: last chunk with mass
-        // level 2: segments of chunk cstar (pairs per lane, warp scan: the main pass's association)
-        const int cl = min(P.CH, P.V - cstar * P.CH);
-        const int cnvv = (cl + VEC - 1) / VEC;
-        const int cnsg = (cnvv + SEGV - 1) / SEGV;
-        const double2* gseg = P.segtab + (static_cast<size_t>(b) * nch + cstar) * P.nseg;
-        const double2 a0 = 2 * lane < cnsg ? __ldcg(gseg + 2 * lane) : make_double2(0.0, 0.0);
-        const double2 a1 = 2 * lane + 1 < cnsg ? __ldcg(gseg + 2 * lane + 1) : make_double2(0.0, 0.0);
-        const double m0 = zero_res ? a0.y : a0.x, m1 = zero_res ? a1.y : a1.x;
-        const double2 ip = warp_scan2(make_double2(__dadd_rn(a0.x, a1.x), __dadd_rn(a0.y, a1.y)), lane);
-        const double ipm = zero_res ? ip.y : ip.x;
-        const unsigned hs = __ballot_sync(0xFFFFFFFFu, ipm > th1);
-        const unsigned ps = __ballot_sync(0xFFFFFFFFu, __dadd_rn(m0, m1) > 0.0);
-        const int lp = hs ? __ffs(hs) - 1 : (ps ? 31 - __clz(ps) : 0);
-        double exs = __shfl_up_sync(0xFFFFFFFFu, ipm, 1);
-        if (lane == 0) exs = 0.0;
-        exs = __shfl_sync(0xFFFFFFFFu, exs, lp);
-        const double lm0 = __shfl_sync(0xFFFFFFFFu, m0, lp), lm1 = __shfl_sync(0xFFFFFFFFu, m1, lp);
-        int sstar;
-        double th2;
-        if (!hs) {                                    // rounding: last segment with mass
-            sstar = lm1 > 0.0 ? 2 * lp + 1 : 2 * lp;
-            th2 = INFINITY;
-        } else if (__dadd_rn(exs, lm0) > th1) {
-            sstar = 2 * lp;
-            th2 = th1 - exs;
-        } else {
-            sstar = 2 * lp + 1;
-            th2 = th1 - __dadd_rn(exs, lm0);
-        }
-        // recompute the segment exactly as the main pass did (r and p terms both; zero_res
-        // selects p)
-        const int g = sstar * SEGV + lane;
-        const int valid = min(VEC, max(0, cl - g * VEC));
-        uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
-        if (g < cnvv) {
-            up = __ldcg(reinterpret_cast<const uint4*>(gp + cstar * P.CH) + g);
-            if (use_q) uq = __ldcg(reinterpret_cast<const uint4*>(gq + cstar * P.CH) + g);
-        }
-        float r[VEC], pv[VEC], sr, spv;
-        resid_terms<E>(up, uq, valid, rp, c2, r, pv, sr, spv);
-        const double2 inc = warp_scan2(make_double2(sr, spv), lane);
-        const double icv = zero_res ? inc.y : inc.x;
-        const float mine = zero_res ? spv : sr;
-        const unsigned hit = __ballot_sync(0xFFFFFFFFu, icv > th2);
-        const unsigned posm = __ballot_sync(0xFFFFFFFFu, mine > 0.0f);
-        const int ls = hit ? __ffs(hit) - 1 : (posm ? 31 - __clz(posm) : 0);
-        double ex = __shfl_up_sync(0xFFFFFFFFu, icv, 1);
-        if (lane == 0) ex = 0.0;
-        int fe = -1;
-        if (lane == ls) {
-            const double th3 = hit ? th2 - ex : INFINITY;
-            int lastpos = -1;
-            float cum = 0.0f;
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-                const float te = zero_res ? pv[e] : r[e];
-                if (te > 0.0f) lastpos = e;
-                cum = e == 0 ? te : __fadd_rn(cum, te);
-                if (fe < 0 && static_cast<double>(cum) > th3) fe = e;
-            }
-            if (fe < 0) fe = lastpos >= 0 ? lastpos : 0;   // rounding: clamp (C-9)
-        }
-        fe = __shfl_sync(0xFFFFFFFFu, fe, ls);
-        tok = cstar * P.CH + (sstar * SEGV + ls) * VEC + fe;
-        if (zero_res) status |= kZeroResidual;
+    // level 1: chunks, one lane each, warp scans over blocks of 32 chunks (carry between blocks)
+    auto chunk_mass = [&](int cc) -> double2 {
+        if (cc >= nch) return make_double2(0.0, 0.0);
+        const PartB t = load_cg(P.partB + static_cast<size_t>(b) * nch + cc);
+        return make_double2(t.R, t.P);
+    };
+    double2 carry = make_double2(0.0, 0.0);
+    for (int base = 0; base < nch; base += 32) {
+        const double2 icb = warp_scan2(chunk_mass(base + lane), lane);
+        carry.x = __dadd_rn(carry.x, __shfl_sync(0xFFFFFFFFu, icb.x, 31));
+        carry.y = __dadd_rn(carry.y, __shfl_sync(0xFFFFFFFFu, icb.y, 31));
     }
-    if (lane == 0) {
-        const int Lout = hard ? 0 : L;
-        P.out_L[b] = Lout;
-        int32_t* ot = P.out_tok + static_cast<size_t>(b) * (kk + 1);
-        for (int i = 0; i <= kk; ++i) {
-            int32_t v = -1;
-            if (!hard) v = i < L ? P.ids[static_cast<size_t>(b) * kk + i] : (i == L ? tok : -1);
-            ot[i] = v;
+    const bool zero_res = use_q && !(carry.x > 0.0);        // C-6: fall back to p_L
+    const double tot = zero_res ? carry.y : carry.x;
+    const uint4 w = verify_words(P.seed, static_cast<uint32_t>(L), P.round,
+                                 P.rid_base + static_cast<uint64_t>(b));
+    const double theta = unit24(w.y) * tot;                 // C-9: first x with C(x) > theta
+    int cstar = -1, clast = 0;
+    double th1 = INFINITY, run = 0.0;
+    for (int base = 0; base < nch && cstar < 0; base += 32) {
+        const double2 pb = chunk_mass(base + lane);
+        const double2 icb = warp_scan2(pb, lane);
+        const double icm = __dadd_rn(run, zero_res ? icb.y : icb.x);
+        const double mcm = zero_res ? pb.y : pb.x;
+        const unsigned h = __ballot_sync(0xFFFFFFFFu, base + lane < nch && icm > theta);
+        const unsigned pm = __ballot_sync(0xFFFFFFFFu, base + lane < nch && mcm > 0.0);
+        if (pm) clast = base + 31 - __clz(pm);
+        if (h) {
+            const int l = __ffs(h) - 1;
+            double e = __shfl_up_sync(0xFFFFFFFFu, icm, 1);
+            if (lane == 0) e = run;
+            cstar = base + l;
+            th1 = theta - __shfl_sync(0xFFFFFFFFu, e, l);
         }
-        if (P.out_status) P.out_status[b] = status;
+        run = __shfl_sync(0xFFFFFFFFu, icm, 31);
+    }
+    if (cstar < 0) cstar = clast;                           // rounding: last chunk with mass
+    // level 2: segments of chunk cstar (pairs per lane, warp scan: the main pass's association)
+    const int cl = min(P.CH, P.V - cstar * P.CH);
+    const int cnvv = (cl + VEC - 1) / VEC;
+    const int cnsg = (cnvv + SEGV - 1) / SEGV;
+    const double2* gseg = P.segtab + (static_cast<size_t>(b) * nch + cstar) * P.nseg;
+    const double2 a0 = 2 * lane < cnsg ? __ldcg(gseg + 2 * lane) : make_double2(0.0, 0.0);
+    const double2 a1 = 2 * lane + 1 < cnsg ? __ldcg(gseg + 2 * lane + 1) : make_double2(0.0, 0.0);
+    const double m0 = zero_res ? a0.y : a0.x, m1 = zero_res ? a1.y : a1.x;
+    const double2 ip = warp_scan2(make_double2(__dadd_rn(a0.x, a1.x), __dadd_rn(a0.y, a1.y)), lane);
+    const double ipm = zero_res ? ip.y : ip.x;
+    const unsigned hs = __ballot_sync(0xFFFFFFFFu, ipm > th1);
+    const unsigned ps = __ballot_sync(0xFFFFFFFFu, __dadd_rn(m0, m1) > 0.0);
+    const int lp = hs ? __ffs(hs) - 1 : (ps ? 31 - __clz(ps) : 0);
+    double exs = __shfl_up_sync(0xFFFFFFFFu, ipm, 1);
+    if (lane == 0) exs = 0.0;
+    exs = __shfl_sync(0xFFFFFFFFu, exs, lp);
+    const double lm0 = __shfl_sync(0xFFFFFFFFu, m0, lp), lm1 = __shfl_sync(0xFFFFFFFFu, m1, lp);
+    int sstar;
+    double th2;
+    if (!hs) {                                    // rounding: last segment with mass
+        sstar = lm1 > 0.0 ? 2 * lp + 1 : 2 * lp;
+        th2 = INFINITY;
+    } else if (__dadd_rn(exs, lm0) > th1) {
+        sstar = 2 * lp;
+        th2 = th1 - exs;
+    } else {
+        sstar = 2 * lp + 1;
+        th2 = th1 - __dadd_rn(exs, lm0);
+    }
+    // recompute the segment exactly as the main pass did (r and p terms both; zero_res selects p)
+    const int g = sstar * SEGV + lane;
+    const int valid = min(VEC, max(0, cl - g * VEC));
+    uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
+    if (g < cnvv) {
+        up = __ldcg(reinterpret_cast<const uint4*>(gp + cstar * P.CH) + g);
+        if (use_q) uq = __ldcg(reinterpret_cast<const uint4*>(gq + cstar * P.CH) + g);
+    }
+    float r[VEC], pv[VEC], sr, spv;
+    resid_terms<E>(up, uq, valid, rp, c2, r, pv, sr, spv);
+    const double2 inc = warp_scan2(make_double2(sr, spv), lane);
+    const double icv = zero_res ? inc.y : inc.x;
+    const float mine = zero_res ? spv : sr;
+    const unsigned hit = __ballot_sync(0xFFFFFFFFu, icv > th2);
+    const unsigned posm = __ballot_sync(0xFFFFFFFFu, mine > 0.0f);
+    const int ls = hit ? __ffs(hit) - 1 : (posm ? 31 - __clz(posm) : 0);
+    double ex = __shfl_up_sync(0xFFFFFFFFu, icv, 1);
+    if (lane == 0) ex = 0.0;
+    int fe = -1;
+    if (lane == ls) {
+        const double th3 = hit ? th2 - ex : INFINITY;
+        int lastpos = -1;
+        float cum = 0.0f;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+            const float te = zero_res ? pv[e] : r[e];
+            if (te > 0.0f) lastpos = e;
+            cum = e == 0 ? te : __fadd_rn(cum, te);
+            if (fe < 0 && static_cast<double>(cum) > th3) fe = e;
+        }
+        if (fe < 0) fe = lastpos >= 0 ? lastpos : 0;   // rounding: clamp (C-9)
+    }
+    fe = __shfl_sync(0xFFFFFFFFu, fe, ls);
+    if (zero_res) status |= kZeroResidual;
+    return cstar * P.CH + (sstar * SEGV + ls) * VEC + fe;
+}
+
+// grid (chunk c, request b): the chunked sampler for rows longer than k_sample_req's on-chip
+// segment table (launched after k_row_stats with programmatic dependent launch).
+template <typename E>
+__global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
+    constexpr int MAXSEG = kMaxChunkBytes / 16 / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ double2 s_seg[MAXSEG];
+    __shared__ int s_last;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int kk = P.k;
+    const int c = blockIdx.x, b = blockIdx.y + blockIdx.z * kGridY;
+    if (b >= P.B) return;   // (whole CTA: the request's tickets count only real CTAs)
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    // programmatic dependent launch: this grid may start while k_row_stats drains; wait until
+    // every row decision of the primary grid is complete and visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint32_t mask = P.rej_mask[b];
+    const int L = mask ? __ffs(mask) - 1 : kk;
+    const RowStat rs = P.rowstat[static_cast<size_t>(b) * (kk + 1) + L];
+    const bool hard = (rs.status & kHard) != 0;
+    __syncthreads();
+    uint32_t ph0 = 0, ph1 = 0;
+    if (!sample_chunk<E>(P, smem, bar, ph0, ph1, s_seg, &s_last, b, L, c, rs, hard) || warp != 0)
+        return;
+    int32_t status = rs.status;
+    const int32_t tok = hard ? -1 : sample_search<E>(P, b, L, rs, status, lane);
+    if (lane == 0) {
+        write_outputs(P, b, L, tok, status, hard);
         P.rej_mask[b] = 0u;      // leave the workspace zeroed for the next call
         P.ticketB[b] = 0u;
         for (int i = 0; i <= kk; ++i) P.ticketA[static_cast<size_t>(b) * (kk + 1) + i] = 0u;
@@ -1444,7 +1506,6 @@ static cudaError_t launch_sampled(const Params& P, cudaStream_t st, cudaEvent_t 
 template <typename E>
 static cudaError_t launch_greedy(const Params& P, cudaStream_t st, cudaEvent_t ev0,
                                  cudaEvent_t ev1) {
-    const size_t smem = static_cast<size_t>(P.CH) * sizeof(E);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_row_stats<E, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
