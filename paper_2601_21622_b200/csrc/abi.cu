@@ -210,15 +210,6 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     P.partA = reinterpret_cast<PartA*>(ws + w.partA);
     P.partB = reinterpret_cast<PartB*>(ws + w.partB);
     P.segtab = reinterpret_cast<double2*>(ws + w.segtab);
-    P.state = reinterpret_cast<unsigned long long*>(ws + w.state);
-    {
-        static int early = -1;   // STARSD_EARLY=0: the sampler waits for the whole stats grid
-        if (early < 0) {
-            const char* e = getenv("STARSD_EARLY");
-            early = (e && strcmp(e, "0") == 0) ? 0 : 1;
-        }
-        P.early = greedy ? 0 : early;
-    }
 
     cudaError_t e = launch_verify(P, greedy, shape->dtype == SD_DTYPE_BF16, stream, ev0, ev1);
     if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));

@@ -66,10 +66,6 @@ struct Params {
     double2* segtab;             // [B][nch][nseg]  (r mass, p mass) per warp segment
     int32_t nseg;                // segments per chunk
     unsigned long long* trace;   // debug builds only (SD_STREAM_DEBUG): per-CTA phase timestamps
-    // early sampler start: k_row_stats triggers its dependent launch at once and the per-request
-    // sampler waits for its own request's stop position instead of the whole primary grid
-    int32_t early;
-    unsigned long long* state;   // [B]  bits 0..k: stop at row j; bits 32..32+k: row j decided
 };
 
 // k_row_stats cluster size for a row of nch chunks: a cluster covers the whole row when nch <= 8
@@ -98,7 +94,7 @@ inline int32_t row_cluster(int32_t nch) {
 // Workspace layout for a shape; all offsets 16-byte aligned.  The first `zero_bytes` must be
 // zero before a call and are zero again after it.
 struct WsLayout {
-    size_t rej_mask, ticketA, ticketB, state, zero_bytes;
+    size_t rej_mask, ticketA, ticketB, zero_bytes;
     size_t rowstat, partA, partB, segtab, total;
 };
 
@@ -123,7 +119,6 @@ inline WsLayout ws_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
     w.rej_mask = o; o = align16(o + sizeof(uint32_t) * B);
     w.ticketA = o;  o = align16(o + sizeof(uint32_t) * (size_t)B * (k + 1));
     w.ticketB = o;  o = align16(o + sizeof(uint32_t) * B);
-    w.state = o;    o = align16(o + sizeof(unsigned long long) * B);
     w.zero_bytes = o;
     w.rowstat = o;  o = align16(o + sizeof(RowStat) * (size_t)B * (k + 1));
     w.partA = o;    o = align16(o + sizeof(PartA) * (size_t)B * (k + 1) * nch);

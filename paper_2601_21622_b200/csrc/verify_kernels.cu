@@ -230,16 +230,6 @@ __device__ __forceinline__ void thread_stats(const float (&v)[NV][VEC], float c2
     s = x0 + x1;
 }
 
-// ---- settling a request's stop position ------------------------------------------------------
-// state[b] collects, per row j, "decided" (bit 32 + j) and "stop" (bit j).  L = the lowest stop
-// (k if none) is settled once rows 0..L are all decided.
-__device__ __forceinline__ bool settled(unsigned long long s, int kk, int& L) {
-    const uint32_t rej = static_cast<uint32_t>(s);
-    L = rej ? __ffs(rej) - 1 : kk;
-    const uint32_t need = L >= 31 ? 0xFFFFFFFFu : ((2u << L) - 1u);
-    return (static_cast<uint32_t>(s >> 32) & need) == need;
-}
-
 // ---- outputs --------------------------------------------------------------------------------
 // out_accept_len / out_tokens / out_status of request b (one thread)
 __device__ __forceinline__ void write_outputs(const Params& P, int b, int L, int32_t tok,
@@ -383,11 +373,6 @@ __device__ __forceinline__ void decide(const Params& P, int b, int j, int x, con
     rs.argmax = C.RG;
     P.rowstat[pos] = rs;
     if (stop) atomicOr(P.rej_mask + b, 1u << j);
-    if (!GREEDY && P.early) {
-        // "row j decided (and stopped)", release: this row's RowStat is visible before it
-        const unsigned long long bits = (1ull << (32 + j)) | (stop ? (1ull << j) : 0ull);
-        asm volatile("red.release.gpu.global.or.b64 [%0], %1;" ::"l"(P.state + b), "l"(bits) : "memory");
-    }
 }
 
 // The last publisher of a row pair combines the row's G published partials (fp64) and takes the
@@ -534,9 +519,6 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
     const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
 
     const int rank = CL > 1 ? c % CL : 0;
-    // the dependent sampler may launch once every CTA of this grid has started (it waits per
-    // request for the stop position, P.early)
-    if (!GREEDY && P.early) asm volatile("griddepcontrol.launch_dependents;");
     if (tid == 0) {
         SD_TR(P, 0);
         const uint32_t m = j ? ld_relaxed_u32(P.rej_mask + b) : 0u;
@@ -1108,7 +1090,6 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
     if (lane == 0) {
         write_outputs(P, b, L, tok, status, hard);
         P.rej_mask[b] = 0u;      // leave the workspace zeroed for the next call
-        P.state[b] = 0ull;
         P.ticketB[b] = 0u;
         for (int i = 0; i <= kk; ++i) P.ticketA[static_cast<size_t>(b) * (kk + 1) + i] = 0u;
     }
@@ -1144,7 +1125,6 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
     __shared__ double s_blk[kSMaxSeg / 32];                   // block (32-segment) masses
     __shared__ double s_th;
     __shared__ int s_sel[2];
-    __shared__ int s_L;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int kk = P.k;
@@ -1158,26 +1138,11 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
         fence_mbar_init();
     }
     if (tid == 0) SD_TRS(P, 0);
-    if (P.early) {
-        // started while k_row_stats may still run: wait for this request's stop position only
-        // (acquire: the RowStat of every decided row is visible)
-        if (tid == 0) {
-            int l = kk;
-            unsigned long long st = 0;
-            SD_SPIN((st = ld_acquire_u64(P.state + b), settled(st, kk, l)), 8);
-            s_L = l;
-        }
-    } else {
-        // programmatic dependent launch: wait until every decision of k_row_stats is visible
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        if (tid == 0) {
-            const uint32_t mask = P.rej_mask[b];
-            s_L = mask ? __ffs(mask) - 1 : kk;
-        }
-    }
-    __syncthreads();
+    // programmatic dependent launch: wait until every decision of k_row_stats is visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (tid == 0) SD_TRS(P, 1);
-    const int L = s_L;
+    const uint32_t mask = P.rej_mask[b];
+    const int L = mask ? __ffs(mask) - 1 : kk;
     const RowStat rs = load_cg(P.rowstat + static_cast<size_t>(b) * (kk + 1) + L);
     const bool hard = (rs.status & kHard) != 0;
     const bool use_q = L < kk;
@@ -1402,11 +1367,7 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
             ot[i] = v;
         }
         if (P.out_status) P.out_status[b] = status;
-        // rows of this request past L may still be in flight in k_row_stats (early start): reset
-        // its decision state only once the primary grid is complete
-        if (P.early) asm volatile("griddepcontrol.wait;" ::: "memory");
         P.rej_mask[b] = 0u;      // leave the workspace zeroed for the next call
-        P.state[b] = 0ull;
         for (int i = 0; i <= kk; ++i) P.ticketA[static_cast<size_t>(b) * (kk + 1) + i] = 0u;
         SD_TRS(P, 2);
     }
