@@ -158,6 +158,18 @@ sd_status sd_philox_uniforms(uint64_t seed, uint64_t round, const uint32_t* pos,
 sd_status sd_profile_events(cudaEvent_t* events, int32_t n_pairs);
 
 /*
+ * sd_profile_timestamps -- device-clock span of the dominant kernel without event nodes (an event
+ * node between two kernels of a captured graph costs microseconds and inflates what it brackets).
+ * After this call, the next n_calls two-launch sd_verify calls on this thread fold %globaltimer
+ * (ns) into device_buf with atomic min: word 2 i = the earliest start of a k_row_stats CTA of call
+ * i (after its dependency wait; the first row's CTAs, which the hardware dispatches first, report),
+ * word 2 i + 1 = the earliest moment one of the first CTAs of the call's second kernel saw
+ * k_row_stats complete (griddepcontrol.wait returned).  device_buf: device, 2 * n_calls
+ * uint64 the caller fills with all-ones before the calls it profiles; NULL / 0 disables.
+ */
+sd_status sd_profile_timestamps(unsigned long long* device_buf, int32_t n_calls);
+
+/*
  * sd_debug_trace -- development instrumentation of the stream variant (library built with
  * STARSD_BUILD_DEBUG=1; otherwise ignored).  When device_buf != NULL, subsequent stream-variant
  * sd_verify calls on this thread write, per CTA, a record log of kSTraceN = 8192 uint64 words:

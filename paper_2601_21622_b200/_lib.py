@@ -21,7 +21,7 @@ STAR_ID_BYTES = 128
 EXPORTS = ["sd_verify", "sd_verify_workspace_size", "sd_philox_uniforms", "sd_star_unique_ids",
            "sd_star_create", "sd_star_round", "sd_star_poll", "sd_star_draft_begin",
            "sd_star_draft_end", "sd_star_stats", "sd_star_destroy", "sd_status_string",
-           "sd_last_error", "sd_version", "sd_profile_events", "sd_debug_trace",
+           "sd_last_error", "sd_version", "sd_profile_events", "sd_profile_timestamps", "sd_debug_trace",
            "sd_star_simulate", "sd_verify_plan"]
 
 
@@ -114,6 +114,8 @@ def load():
     L.sd_star_simulate.restype = st
     L.sd_profile_events.argtypes = [vp, i32]
     L.sd_profile_events.restype = st
+    L.sd_profile_timestamps.argtypes = [vp, i32]
+    L.sd_profile_timestamps.restype = st
     L.sd_debug_trace.argtypes = [vp]
     L.sd_debug_trace.restype = st
     L.sd_status_string.argtypes = [st]

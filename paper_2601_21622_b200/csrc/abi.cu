@@ -22,6 +22,8 @@ cudaError_t launch_philox(uint64_t seed, uint64_t round, const uint32_t* pos, co
 static thread_local char g_err[512] = "";
 static thread_local cudaEvent_t* g_prof_ev = nullptr;
 static thread_local int32_t g_prof_n = 0, g_prof_i = 0;
+static thread_local unsigned long long* g_ts = nullptr;
+static thread_local int32_t g_ts_n = 0, g_ts_i = 0;
 static thread_local unsigned long long* g_trace = nullptr;
 
 sd_status fail(sd_status s, const char* fmt, ...) {
@@ -201,6 +203,16 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     P.rid_base = request_id_base;
     P.out_L = out_accept_len;
     P.trace = g_trace;
+    P.prof_ts = nullptr;
+    if (g_ts && g_ts_i < g_ts_n) P.prof_ts = g_ts + 2 * static_cast<size_t>(g_ts_i++);
+    {
+        static int chain = -1;   // STARSD_CHAIN=0: plain stream order before k_row_stats
+        if (chain < 0) {
+            const char* e = getenv("STARSD_CHAIN");
+            chain = (e && strcmp(e, "0") == 0) ? 0 : 1;
+        }
+        P.chain = chain;
+    }
     P.out_tok = out_tokens;
     P.out_status = out_status;
     P.rej_mask = reinterpret_cast<uint32_t*>(ws + w.rej_mask);
@@ -266,6 +278,16 @@ sd_status sd_profile_events(cudaEvent_t* events, int32_t n_pairs) {
     g_prof_ev = n_pairs ? events : nullptr;
     g_prof_n = n_pairs;
     g_prof_i = 0;
+    return SD_OK;
+}
+
+sd_status sd_profile_timestamps(unsigned long long* device_buf, int32_t n_calls) {
+    clear_error();
+    if (n_calls < 0 || (n_calls > 0 && !device_buf))
+        return fail(SD_ERR_INVALID_ARGUMENT, "device_buf / n_calls");
+    g_ts = n_calls ? device_buf : nullptr;
+    g_ts_n = n_calls;
+    g_ts_i = 0;
     return SD_OK;
 }
 

@@ -66,6 +66,9 @@ struct Params {
     double2* segtab;             // [B][nch][nseg]  (r mass, p mass) per warp segment
     int32_t nseg;                // segments per chunk
     unsigned long long* trace;   // debug builds only (SD_STREAM_DEBUG): per-CTA phase timestamps
+    unsigned long long* prof_ts; // sd_profile_timestamps: [2] this call's span words, or NULL
+    int32_t chain;               // k_row_stats launched as a programmatic dependent of whatever
+                                 // kernel precedes it on the stream (griddepcontrol.wait first)
 };
 
 // k_row_stats cluster size for a row of nch chunks: a cluster covers the whole row when nch <= 8

@@ -230,6 +230,13 @@ __device__ __forceinline__ void thread_stats(const float (&v)[NV][VEC], float c2
     s = x0 + x1;
 }
 
+// ---- sd_profile_timestamps: fold %globaltimer into a span word (atomic min, no return) -------
+__device__ __forceinline__ void prof_min(unsigned long long* w) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(w), "l"(t) : "memory");
+}
+
 // ---- outputs --------------------------------------------------------------------------------
 // out_accept_len / out_tokens / out_status of request b (one thread)
 __device__ __forceinline__ void write_outputs(const Params& P, int b, int L, int32_t tok,
@@ -519,6 +526,11 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
     const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
 
     const int rank = CL > 1 ? c % CL : 0;
+    // launched as a programmatic dependent of the previous kernel on the stream (P.chain): its
+    // results (the previous call's workspace reset, the caller's logits) are visible after this
+    if (P.chain) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // (the earliest CTAs are the first row's: only they fold their start in)
+    if (P.prof_ts && tid == 0 && blockIdx.y == 0 && blockIdx.z == 0) prof_min(P.prof_ts);
     if (tid == 0) {
         SD_TR(P, 0);
         const uint32_t m = j ? ld_relaxed_u32(P.rej_mask + b) : 0u;
@@ -1077,6 +1089,9 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
     // programmatic dependent launch: this grid may start while k_row_stats drains; wait until
     // every row decision of the primary grid is complete and visible
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (P.prof_ts && tid == 0 && blockIdx.x < 8) prof_min(P.prof_ts + 1);
+    // the next call's k_row_stats may be scheduled now (it waits for this grid to complete)
+    if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
     const uint32_t mask = P.rej_mask[b];
     const int L = mask ? __ffs(mask) - 1 : kk;
     const RowStat rs = P.rowstat[static_cast<size_t>(b) * (kk + 1) + L];
@@ -1140,6 +1155,9 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
     if (tid == 0) SD_TRS(P, 0);
     // programmatic dependent launch: wait until every decision of k_row_stats is visible
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (P.prof_ts && tid == 0 && blockIdx.x < 8) prof_min(P.prof_ts + 1);
+    // the next call's k_row_stats may be scheduled now (it waits for this grid to complete)
+    if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
     if (tid == 0) SD_TRS(P, 1);
     const uint32_t mask = P.rej_mask[b];
     const int L = mask ? __ffs(mask) - 1 : kk;
@@ -1377,6 +1395,8 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
 // Greedy finalize: one thread per request
 __global__ void k_finalize_greedy(const Params P) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (P.prof_ts && threadIdx.x == 0 && blockIdx.x < 8) prof_min(P.prof_ts + 1);
+    if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= P.B) return;
     const int kk = P.k;
@@ -1442,22 +1462,27 @@ static void launch_stats_cl(const Params& P, cudaStream_t st) {
     const int nb = (P.B + kGridY - 1) / kGridY;
     const dim3 gridA(CL > 1 ? P.G * CL : P.nch, P.B < kGridY ? P.B : kGridY, (P.k + 1) * nb);
     const size_t sm = (G ? 1 : 2) * static_cast<size_t>(P.CH) * sizeof(E);
-    if (CL == 1) {
-        k_row_stats<E, G, CL><<<gridA, kThreads, sm, st>>>(P);
-        return;
-    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = gridA;
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = sm;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (P.chain) {   // overlap this launch with the tail of the previous kernel on the stream
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (CL > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = CL;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     cudaLaunchKernelEx(&cfg, k_row_stats<E, G, CL>, P);
 }
 template <typename E, bool G>

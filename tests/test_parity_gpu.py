@@ -311,3 +311,32 @@ def test_parity_extreme_temperatures(T):
     """Very peaked (T = 0.05: c2 = log2(e)/T ~ 29) and very flat (T = 5) distributions."""
     d = make_batch(V=32000, k=5, B=32, T=T, kappa=30.0, seed=int(T * 1000) + 7)
     check(d, T, max_tie_frac=2e-2)
+
+
+def test_profile_timestamps_bracket_the_stats_kernel():
+    """sd_profile_timestamps (bench.py's roofline clock): for each profiled call, the earliest
+    k_row_stats CTA start precedes the moment the second kernel saw it complete, by a plausible
+    span; unprofiled calls leave the buffer untouched."""
+    import ctypes
+    from paper_2601_21622_b200 import _lib
+    d = make_batch(V=32000, k=5, B=16, T=1.0, kappa=30.0, seed=77)
+    dev = torch.device("cuda:0")
+    p, q, ids = (torch.from_numpy(d[x]).to(dev) for x in ("p", "q", "ids"))
+    ts = torch.full((3, 2), -1, dtype=torch.int64, device=dev)
+    L = _lib.load()
+    _lib.check(L.sd_profile_timestamps(ctypes.c_void_p(ts.data_ptr()), 2), "sd_profile_timestamps")
+    try:
+        sd.verify(p, q, ids, 1.0, seed=1, round=0)      # profiled: slot 0
+        sd.verify(p, None, ids, 0.0, seed=1, round=0)   # profiled: slot 1 (greedy finalizer)
+        sd.verify(p, q, ids, 1.0, seed=1, round=1)      # past n_calls: not profiled
+    finally:
+        _lib.check(L.sd_profile_timestamps(None, 0), "sd_profile_timestamps")
+    torch.cuda.synchronize()
+    t = ts.cpu().numpy().view(np.uint64)
+    for i in range(2):                               # the sampled call and the greedy call
+        assert t[i, 0] != np.uint64(2**64 - 1) and t[i, 1] != np.uint64(2**64 - 1)
+        span = int(t[i, 1]) - int(t[i, 0])
+        assert 0 < span < 10_000_000, span           # ns
+    assert (t[2] == np.uint64(2**64 - 1)).all()      # only n_calls calls are profiled
+    with pytest.raises(sd.StarsdError):
+        _lib.check(L.sd_profile_timestamps(None, 3), "sd_profile_timestamps")
