@@ -1186,9 +1186,9 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
         float rho = use_q ? static_cast<float>(rs.S_p / rs.S_q) : -1.0f;   // < 0: p only
         bool zero_res = false;
         for (int attempt = 0; attempt < 2; ++attempt) {
-            // ---- stream the row: unit u in slot u % kSRing --------------------------------
-            auto issue = [&](int u) {
-                const int sl = u % kSRing;
+            // ---- stream the row: unit u at ring position n (slot n % kSRing) ----------------
+            auto issue = [&](int n, int u) {
+                const int sl = n % kSRing;
                 const uint32_t off = static_cast<uint32_t>(u) * kSUnitBytes;
                 const uint32_t nb = min(static_cast<uint32_t>(kSUnitBytes), rowbytes - off);
                 unsigned char* dst = smem + static_cast<size_t>(sl) * 2 * kSUnitBytes;
@@ -1208,7 +1208,7 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
                 for (int u = 0; u < nunits; ++u) {
                     const int n = base_u + u;
                     if (n >= kSRing) mbar_wait(&empty[n % kSRing], ((n / kSRing) & 1) ^ 1);
-                    issue(n);
+                    issue(n, u);   // (the retry pass re-reads units 0.. at later ring positions)
                 }
             } else {
                 for (int u = 0; u < nunits; ++u) {
