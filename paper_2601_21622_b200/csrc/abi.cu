@@ -204,6 +204,16 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     P.out_L = out_accept_len;
     P.trace = g_trace;
     P.prof_ts = nullptr;
+    P.epoch = reinterpret_cast<uint32_t*>(ws + w.epoch);
+    P.partT = reinterpret_cast<unsigned long long*>(ws + w.partT);
+    {
+        static int tag = -1;   // STARSD_PUBLISH=ticket: release-ordered partials + row ticket
+        if (tag < 0) {
+            const char* e = getenv("STARSD_PUBLISH");
+            tag = (e && strcmp(e, "ticket") == 0) ? 0 : 1;
+        }
+        P.tagpub = (tag && P.CL == 1 && P.nch >= 2 && P.nch <= kMaxTagNch) ? 1 : 0;
+    }
     if (g_ts && g_ts_i < g_ts_n) P.prof_ts = g_ts + 2 * static_cast<size_t>(g_ts_i++);
     {
         static int chain = -1;   // STARSD_CHAIN=0: plain stream order before k_row_stats

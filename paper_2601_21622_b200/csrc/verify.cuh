@@ -13,6 +13,7 @@ constexpr int kVecBytes = 16;            // one 128-bit smem/global vector per t
 constexpr int kTileBytes = kThreads * kVecBytes;   // 4 KB of one row per tile
 constexpr int kMaxChunkBytes = 16 * 1024;          // one CTA owns <= 16 KB of a row (measured best of 8/16/32 KB)
 constexpr int kRowClusterDefault = 8;              // see row_cluster()
+constexpr int kMaxTagNch = 64;                     // tagged partials: rows of at most 64 chunks
 
 // Per (request b, position j, vocab chunk c): what one kernel-A CTA found in its slice.
 struct PartA {
@@ -67,6 +68,12 @@ struct Params {
     int32_t nseg;                // segments per chunk
     unsigned long long* trace;   // debug builds only (SD_STREAM_DEBUG): per-CTA phase timestamps
     unsigned long long* prof_ts; // sd_profile_timestamps: [2] this call's span words, or NULL
+    // tagged partials (tagpub, rows of 2..kMaxTagNch chunks without clusters): every word of a
+    // chunk partial carries the call's tag, so a CTA publishes with plain stores and exits; the
+    // row's last chunk CTA polls the words of the others and decides (no fence, no ticket)
+    int32_t tagpub;
+    uint32_t* epoch;             // [1]  calls completed on this workspace (tag = epoch + 1)
+    unsigned long long* partT;   // [B][k+1][nch][5 * 2]  tag << 32 | 32 data bits
     int32_t chain;               // k_row_stats launched as a programmatic dependent of whatever
                                  // kernel precedes it on the stream (griddepcontrol.wait first)
 };
@@ -97,8 +104,8 @@ inline int32_t row_cluster(int32_t nch) {
 // Workspace layout for a shape; all offsets 16-byte aligned.  The first `zero_bytes` must be
 // zero before a call and are zero again after it.
 struct WsLayout {
-    size_t rej_mask, ticketA, ticketB, zero_bytes;
-    size_t rowstat, partA, partB, segtab, total;
+    size_t rej_mask, ticketA, ticketB, epoch, zero_bytes;
+    size_t rowstat, partA, partB, segtab, partT, total;
 };
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -122,11 +129,14 @@ inline WsLayout ws_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
     w.rej_mask = o; o = align16(o + sizeof(uint32_t) * B);
     w.ticketA = o;  o = align16(o + sizeof(uint32_t) * (size_t)B * (k + 1));
     w.ticketB = o;  o = align16(o + sizeof(uint32_t) * B);
+    w.epoch = o;    o = align16(o + sizeof(uint32_t));
     w.zero_bytes = o;
     w.rowstat = o;  o = align16(o + sizeof(RowStat) * (size_t)B * (k + 1));
     w.partA = o;    o = align16(o + sizeof(PartA) * (size_t)B * (k + 1) * nch);
     w.partB = o;    o = align16(o + sizeof(PartB) * (size_t)B * nch);
     w.segtab = o;   o = align16(o + sizeof(double) * 2 * (size_t)B * nch * nseg);
+    w.partT = o;
+    if (nch >= 2 && nch <= kMaxTagNch) o = align16(o + 80 * (size_t)B * (k + 1) * nch);
     w.total = o;
     return w;
 }

@@ -431,6 +431,36 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define SD_TRS(P, i) do {} while (0)
 #endif
 
+// ---- tagged partials (k_row_stats with P.tagpub) --------------------------------------------
+// A chunk partial is ten 32-bit words, each stored as one 8-byte word tag << 32 | data (single-copy
+// atomic), so a reader that sees the call's tag in all ten has the whole partial without any
+// fence on the writer's side.
+__device__ __forceinline__ void write_tagged(const Params& P, size_t pos, int c, const PartA& a,
+                                             uint32_t tag) {
+    static_assert(sizeof(PartA) == 40, "PartA is ten 32-bit words");
+    unsigned long long* w = P.partT + (pos * P.nch + c) * 10;
+    const uint32_t* d = reinterpret_cast<const uint32_t*>(&a);
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        const unsigned long long v = (static_cast<unsigned long long>(tag) << 32) | d[i];
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(w + i), "l"(v) : "memory");
+    }
+}
+__device__ __forceinline__ bool read_tagged(const Params& P, size_t pos, int c, uint32_t tag,
+                                            PartA& a) {
+    const unsigned long long* w = P.partT + (pos * P.nch + c) * 10;
+    uint32_t* d = reinterpret_cast<uint32_t*>(&a);
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        unsigned long long v;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(w + i) : "memory");
+        ok = ok && static_cast<uint32_t>(v >> 32) == tag;
+        d[i] = static_cast<uint32_t>(v);
+    }
+    return ok;
+}
+
 // ---- cluster publish (k_row_stats with CL > 1) --------------------------------------------
 // A peer's partial goes into the leader's slot with five asynchronous 8-byte stores that complete
 // transaction bytes on the leader's s_pbar (armed for (CL-1) * 40 bytes): no release fence.
@@ -505,6 +535,8 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ __align__(8) uint64_t s_pbar;                    // CL > 1, leader: peer partials
     __shared__ __align__(16) PartA s_parts[CL];
+    __shared__ __align__(16) PartA s_all[kMaxTagNch];          // P.tagpub: the row's partials
+    __shared__ uint32_t s_tag;
     __shared__ int s_flag;
     __shared__ float s_d[2][kWarps];
     __shared__ double s_s[2][kWarps];
@@ -534,6 +566,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
     if (tid == 0) {
         SD_TR(P, 0);
         const uint32_t m = j ? ld_relaxed_u32(P.rej_mask + b) : 0u;
+        if (P.tagpub) s_tag = ld_relaxed_u32(P.epoch) + 1u;
         s_flag = (m & ((1u << j) - 1u)) != 0u;
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -564,6 +597,12 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
                 } else {
                     SD_SPIN(mbar_try_wait_cluster(&s_pbar, 0), 2);
                 }
+            }
+            // tagged partials: the row's decider (last chunk) may be working -- say "skipped"
+            if (P.tagpub && c != nch - 1) {
+                PartA a{};
+                a.flags = kPartSkipped;
+                write_tagged(P, pos, c, a, s_tag);
             }
         }
         return;
@@ -693,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
     }
     __syncthreads();
     if (tid == 0) SD_TR(P, 4);
-    if (CL > 1 && warp != 0) return;
+    if ((CL > 1 || P.tagpub) && warp != 0) return;
     if (warp == 0) {
         const bool on = lane < kWarps;
         const int f = __reduce_or_sync(0xFFFFFFFFu, on ? s_f[lane] : 0);
@@ -728,6 +767,31 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
         }
         if (CL > 1) {
             cluster_publish<GREEDY, CL>(P, pa, s_parts, &s_pbar, rank, c / CL, b, j, x, lane);
+            return;
+        }
+        if (P.tagpub) {
+            const uint32_t tag = s_tag;
+            if (c != nch - 1) {   // plain tagged stores, then exit: no fence, no ticket
+                if (lane == 0) {
+                    write_tagged(P, pos, c, pa, tag);
+                    SD_TR(P, 5);
+                    SD_TR(P, 6);
+                    SD_TRF(P, 0);
+                }
+                return;
+            }
+            // the row's last chunk decides: the other chunks of the row were dispatched before it
+            if (lane == 0) s_all[c] = pa;
+            for (int cc = lane; cc < nch - 1; cc += 32) {
+                PartA a;
+                SD_SPIN(read_tagged(P, pos, cc, tag, a), 9);
+                s_all[cc] = a;
+            }
+            __syncwarp();
+            const Comb C = combine_parts<GREEDY, true>(s_all, nch, lane);
+            if (lane == 0) SD_TR(P, 5);
+            if (!(C.flags & kPartSkipped) && lane == 0) decide<GREEDY>(P, b, j, x, C);
+            if (lane == 0) { SD_TR(P, 6); SD_TRF(P, 2); }
             return;
         }
         if (lane == 0) {
@@ -1090,6 +1154,8 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
     // every row decision of the primary grid is complete and visible
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (P.prof_ts && tid == 0 && blockIdx.x < 8) prof_min(P.prof_ts + 1);
+    if (P.tagpub && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        P.epoch[0] += 1u;   // k_row_stats is complete: the next call tags with a new value
     // the next call's k_row_stats may be scheduled now (it waits for this grid to complete)
     if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
     const uint32_t mask = P.rej_mask[b];
@@ -1156,6 +1222,8 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
     // programmatic dependent launch: wait until every decision of k_row_stats is visible
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (P.prof_ts && tid == 0 && blockIdx.x < 8) prof_min(P.prof_ts + 1);
+    if (P.tagpub && tid == 0 && blockIdx.x == 0)
+        P.epoch[0] += 1u;   // k_row_stats is complete: the next call tags with a new value
     // the next call's k_row_stats may be scheduled now (it waits for this grid to complete)
     if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
     if (tid == 0) SD_TRS(P, 1);
@@ -1396,6 +1464,8 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
 __global__ void k_finalize_greedy(const Params P) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (P.prof_ts && threadIdx.x == 0 && blockIdx.x < 8) prof_min(P.prof_ts + 1);
+    if (P.tagpub && threadIdx.x == 0 && blockIdx.x == 0)
+        P.epoch[0] += 1u;   // k_row_stats is complete: the next call tags with a new value
     if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= P.B) return;
