@@ -232,12 +232,13 @@ def test_gpu_monte_carlo_matches_exact_outcome():
     ({"STARSD_ROWCLUSTER": "1"}, ("two_launch", 0)),        # cluster-free k_row_stats
     ({"STARSD_ROWCLUSTER": "-8"}, ("two_launch", 8)),       # clusters of 8 on every row (G > 1)
     ({"STARSD_ROWCLUSTER": "-2"}, ("two_launch", 2)),
+    ({"STARSD_PUBLISH": "ticket"}, ("two_launch", 0)),     # release-ordered partials + row ticket
 ])
 def test_kernel_variants_match_the_oracle(env, want):
     """Kernel variants chosen by environment (once per process, so in a subprocess) against the
     oracle on the default path's cases plus a Llama-3-vocabulary case: the opt-in persistent
-    stream kernel, the cluster-free k_row_stats, and forced clusters whose row partials meet
-    through the global ticket (G = ceil(nch / CL) > 1)."""
+    stream kernel, the cluster-free k_row_stats (tagged partials), forced clusters whose row
+    partials meet through the global ticket (G = ceil(nch / CL) > 1), and the ticket publish."""
     import json
     import subprocess
     import sys
