@@ -99,7 +99,10 @@ typedef struct {
  *   out_tokens    device, [B][k+1] int32: x_0..x_{L-1}, then t, then -1 padding
  *   out_status    device, [B] int32 fault bitmask, or NULL
  *   workspace     device, >= sd_verify_workspace_size() bytes, 16-byte aligned, zero-filled
- *                 once before first use; every call leaves it zero-filled again.  One
+ *                 once before first use.  Every call leaves the zero region of its shape
+ *                 zeroed again (word 0 excepted: a call counter the kernels keep, any value is
+ *                 valid), so calls of one shape (batch, k, vocab, dtype, T == 0 or not) reuse it
+ *                 as is; before a call of another shape it must be zero-filled again.  One
  *                 workspace must not be used by two calls that may run concurrently.
  *   stream        CUDA stream the work is ordered on
  * Returns SD_OK (work enqueued), SD_ERR_INVALID_ARGUMENT, or SD_ERR_CUDA (launch failure).

@@ -72,7 +72,8 @@ struct Params {
     // chunk partial carries the call's tag, so a CTA publishes with plain stores and exits; the
     // row's last chunk CTA polls the words of the others and decides (no fence, no ticket)
     int32_t tagpub;
-    uint32_t* epoch;             // [1]  calls completed on this workspace (tag = epoch + 1)
+    uint32_t* epoch;             // [1]  workspace word 0: calls completed on this workspace
+                                 //      (tag = (epoch + 1) | 2^31, never a small integer)
     unsigned long long* partT;   // [B][k+1][nch][5 * 2]  tag << 32 | 32 data bits
     int32_t chain;               // k_row_stats launched as a programmatic dependent of whatever
                                  // kernel precedes it on the stream (griddepcontrol.wait first)
@@ -126,10 +127,10 @@ inline WsLayout ws_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
     const int64_t nseg = CH / (32 * (kVecBytes / esz));   // 32-vector segments per chunk
     WsLayout w{};
     size_t o = 0;
+    w.epoch = o;    o = align16(o + sizeof(uint32_t));   // fixed offset 0 for every shape
     w.rej_mask = o; o = align16(o + sizeof(uint32_t) * B);
     w.ticketA = o;  o = align16(o + sizeof(uint32_t) * (size_t)B * (k + 1));
     w.ticketB = o;  o = align16(o + sizeof(uint32_t) * B);
-    w.epoch = o;    o = align16(o + sizeof(uint32_t));
     w.zero_bytes = o;
     w.rowstat = o;  o = align16(o + sizeof(RowStat) * (size_t)B * (k + 1));
     w.partA = o;    o = align16(o + sizeof(PartA) * (size_t)B * (k + 1) * nch);

@@ -526,7 +526,7 @@ __device__ __forceinline__ void cluster_publish(const Params& P, const PartA& pa
 // combines the CL partials; with G == 1 it decides at once, else it publishes the cluster partial
 // and takes the row ticket (the last of the G leaders decides).  Every CTA of a cluster arrives
 // exactly once, also when it skips, so the leader outlives every remote write into it.
-template <typename E, bool GREEDY, int CL>
+template <typename E, bool GREEDY, int CL, bool TAG>
 __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
     using EL = Elt<E>;
     constexpr int VEC = EL::VEC;
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ __align__(8) uint64_t s_pbar;                    // CL > 1, leader: peer partials
     __shared__ __align__(16) PartA s_parts[CL];
-    __shared__ __align__(16) PartA s_all[kMaxTagNch];          // P.tagpub: the row's partials
+    __shared__ __align__(16) PartA s_all[TAG ? kMaxTagNch : 1]; // TAG: the row's partials
     __shared__ uint32_t s_tag;
     __shared__ int s_flag;
     __shared__ float s_d[2][kWarps];
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
     if (tid == 0) {
         SD_TR(P, 0);
         const uint32_t m = j ? ld_relaxed_u32(P.rej_mask + b) : 0u;
-        if (P.tagpub) s_tag = ld_relaxed_u32(P.epoch) + 1u;
+        if (TAG) s_tag = (ld_relaxed_u32(P.epoch) + 1u) | 0x80000000u;
         s_flag = (m & ((1u << j) - 1u)) != 0u;
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
                 }
             }
             // tagged partials: the row's decider (last chunk) may be working -- say "skipped"
-            if (P.tagpub && c != nch - 1) {
+            if (TAG && c != nch - 1) {
                 PartA a{};
                 a.flags = kPartSkipped;
                 write_tagged(P, pos, c, a, s_tag);
@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
     }
     __syncthreads();
     if (tid == 0) SD_TR(P, 4);
-    if ((CL > 1 || P.tagpub) && warp != 0) return;
+    if ((CL > 1 || TAG) && warp != 0) return;
     if (warp == 0) {
         const bool on = lane < kWarps;
         const int f = __reduce_or_sync(0xFFFFFFFFu, on ? s_f[lane] : 0);
@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
             cluster_publish<GREEDY, CL>(P, pa, s_parts, &s_pbar, rank, c / CL, b, j, x, lane);
             return;
         }
-        if (P.tagpub) {
+        if (TAG) {
             const uint32_t tag = s_tag;
             if (c != nch - 1) {   // plain tagged stores, then exit: no fence, no ticket
                 if (lane == 0) {
@@ -1527,7 +1527,7 @@ void record_event(cudaEvent_t ev, cudaStream_t st) {
     else
         cudaEventRecord(ev, st);
 }
-template <typename E, bool G, int CL>
+template <typename E, bool G, int CL, bool TAG = false>
 static void launch_stats_cl(const Params& P, cudaStream_t st) {
     const int nb = (P.B + kGridY - 1) / kGridY;
     const dim3 gridA(CL > 1 ? P.G * CL : P.nch, P.B < kGridY ? P.B : kGridY, (P.k + 1) * nb);
@@ -1553,10 +1553,14 @@ static void launch_stats_cl(const Params& P, cudaStream_t st) {
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    cudaLaunchKernelEx(&cfg, k_row_stats<E, G, CL>, P);
+    cudaLaunchKernelEx(&cfg, k_row_stats<E, G, CL, TAG>, P);
 }
 template <typename E, bool G>
 static void launch_stats(const Params& P, cudaStream_t st) {
+    if (!G && P.tagpub) {   // (tagged partials: sampled rows without clusters)
+        launch_stats_cl<E, G, 1, !G>(P, st);
+        return;
+    }
     switch (P.CL) {
         case 8: launch_stats_cl<E, G, 8>(P, st); break;
         case 4: launch_stats_cl<E, G, 4>(P, st); break;
@@ -1571,7 +1575,7 @@ static cudaError_t launch_sampled(const Params& P, cudaStream_t st, cudaEvent_t 
     const size_t smem = 2 * static_cast<size_t>(P.CH) * sizeof(E);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_row_stats<E, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_row_stats<E, false, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kMaxChunkBytes * 2);
         cudaFuncSetAttribute(k_sample<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kMaxChunkBytes * 2);
@@ -1603,7 +1607,7 @@ static cudaError_t launch_greedy(const Params& P, cudaStream_t st, cudaEvent_t e
                                  cudaEvent_t ev1) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_row_stats<E, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_row_stats<E, true, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kMaxChunkBytes * 2);
         attr = true;
     }

@@ -202,7 +202,8 @@ def test_workspace_left_zeroed_and_deterministic():
     for o in outs[1:]:
         for a, b in zip(o, outs[0]):
             assert torch.equal(a, b)
-    assert int(ws.buf[:64 * 4 * 8].abs().sum()) == 0   # rej masks and tickets are zero again
+    assert int(ws.buf[16:64 * 4 * 8].abs().sum()) == 0  # rej masks and tickets are zero again
+    # (bytes 0..15: the call counter tagged partials derive their tags from)
 
 
 def test_gpu_monte_carlo_matches_exact_outcome():
@@ -341,3 +342,26 @@ def test_profile_timestamps_bracket_the_stats_kernel():
     assert (t[2] == np.uint64(2**64 - 1)).all()      # only n_calls calls are profiled
     with pytest.raises(sd.StarsdError):
         _lib.check(L.sd_profile_timestamps(None, 3), "sd_profile_timestamps")
+
+
+def test_one_workspace_serves_shapes_of_different_layout():
+    """A workspace sized for a large shape serves smaller shapes of a different layout (tagged
+    partials, clusters, tickets) once it is zero-filled again between shapes (include/starsd.h:
+    each call leaves only its own shape's zero region zeroed); calls of one shape reuse it as is."""
+    ws = sd.Workspace(16, 7, 128256, 1.0, device=DEV)
+    cases = [(128256, 7, 16, 1.0), (128256, 7, 16, 1.0), (60000, 3, 8, 1.0), (32000, 5, 12, 1.0),
+             (128256, 7, 16, 0.0), (300000, 2, 2, 1.0), (128256, 7, 16, 1.0)]
+    prev = None
+    for i, (V, k, B, T) in enumerate(cases):
+        if prev is not None and prev != (V, k, B, T == 0.0):
+            ws.buf.zero_()
+        prev = (V, k, B, T == 0.0)
+        d = make_batch(V=V, k=k, B=B, T=max(T, 1e-3), kappa=30.0, seed=900 + i)
+        p, q, ids = (torch.from_numpy(d[x]).to(DEV) for x in ("p", "q", "ids"))
+        assert sd.workspace_size(B, k, V, T) <= ws.nbytes
+        L, tok, st = sd.verify(p, q if T > 0 else None, ids, T, seed=4, round=i, workspace=ws)
+        torch.cuda.synchronize()
+        ref = oracle.verify(d["p"], d["q"] if T > 0 else None, d["ids"], T, seed=4, round=i,
+                            trace=True, n_threads=8)
+        stats = compare(d, (L.cpu().numpy(), tok.cpu().numpy(), st.cpu().numpy()), ref, T, 4, i, 0)
+        assert stats["ties"] <= max(1, 2e-2 * stats["n"]), stats
