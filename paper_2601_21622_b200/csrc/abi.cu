@@ -212,8 +212,7 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
             const char* e = getenv("STARSD_PUBLISH");
             tag = (e && strcmp(e, "ticket") == 0) ? 0 : 1;
         }
-        // (greedy rows measured faster with the ticket: 55 vs 61 us at c3g)
-        P.tagpub = (tag && !greedy && P.CL == 1 && P.nch >= 2 && P.nch <= kMaxTagNch) ? 1 : 0;
+        P.tagpub = (tag && P.CL == 1 && P.nch >= 2 && P.nch <= kMaxTagNch) ? 1 : 0;
     }
     if (g_ts && g_ts_i < g_ts_n) P.prof_ts = g_ts + 2 * static_cast<size_t>(g_ts_i++);
     {

@@ -527,7 +527,7 @@ __device__ __forceinline__ void cluster_publish(const Params& P, const PartA& pa
 // and takes the row ticket (the last of the G leaders decides).  Every CTA of a cluster arrives
 // exactly once, also when it skips, so the leader outlives every remote write into it.
 template <typename E, bool GREEDY, int CL, bool TAG>
-__global__ void __launch_bounds__(kThreads, 6) k_row_stats(const Params P) {
+__global__ void __launch_bounds__(kThreads, GREEDY ? 8 : 6) k_row_stats(const Params P) {
     using EL = Elt<E>;
     constexpr int VEC = EL::VEC;
     constexpr int NV = kMaxChunkBytes / kVecBytes / kThreads;   // 16-byte vectors per thread
@@ -1557,8 +1557,8 @@ static void launch_stats_cl(const Params& P, cudaStream_t st) {
 }
 template <typename E, bool G>
 static void launch_stats(const Params& P, cudaStream_t st) {
-    if (!G && P.tagpub) {   // (tagged partials: sampled rows without clusters)
-        launch_stats_cl<E, G, 1, !G>(P, st);
+    if (P.tagpub) {   // (tagged partials: rows of 9..64 chunks without clusters)
+        launch_stats_cl<E, G, 1, true>(P, st);
         return;
     }
     switch (P.CL) {
