@@ -1186,7 +1186,8 @@ __global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
 // memory, and searches blocks of 32 segments -> segment -> lane -> token on chip; only the found
 // segment is re-read (32 vectors).  No ticket, no global segment table.
 constexpr int kSThreadsB = 512;
-constexpr int kSRing = 3;                         // ring slots (p unit | q unit each)
+constexpr int kSRing = 3;                         // ring slots (p unit | q unit each); 6 slots of
+                                                  // 16 KB units measured 1-3 % slower (c2, c3)
 constexpr int kSUnitBytes = 32 * 1024;            // bytes of p (and of q) per unit: one bulk copy
                                                   // per issuing thread (tools/tma_probe)
 constexpr int kSMaxSeg = 2048;                    // segments per row kept in shared memory
@@ -1284,15 +1285,17 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
                     const uint32_t ph = (n / kSRing) & 1;
                     mbar_wait(&full[sl][0], ph);
                     if (rp.use_q) mbar_wait(&full[sl][1], ph);
+                    if (tid == 0 && u == 0 && attempt == 0) SD_TRS(P, 3);
                     const uint4* sp4 = reinterpret_cast<const uint4*>(smem + static_cast<size_t>(sl) * 2 * kSUnitBytes);
                     const uint4* sq4 = sp4 + UV;
-                    // warp w: segments 4w .. 4w+3 of the unit (one vector per lane each), then one
-                    // transpose-reduce of the four fp64 masses (12 shuffles instead of 40)
-                    static_assert(USEG == 4 * NW, "four segments per consumer warp and unit");
-                    double d[4];
+                    // warp w: segments SPW*w .. SPW*w+SPW-1 of the unit (one vector per lane
+                    // each), then one transpose-reduce of the SPW fp64 masses
+                    constexpr int SPW = USEG / NW;
+                    static_assert(SPW == 2 || SPW == 4, "two or four segments per consumer warp");
+                    double d[SPW];
 #pragma unroll
-                    for (int k4 = 0; k4 < 4; ++k4) {
-                        const int sg = 4 * warp + k4;
+                    for (int k4 = 0; k4 < SPW; ++k4) {
+                        const int sg = SPW * warp + k4;
                         const int g = u * UV + sg * SEGV + lane;    // row vector index
                         uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
                         if (g < nvv) {
@@ -1303,21 +1306,33 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
                         float r[VEC];
                         d[k4] = static_cast<double>(resid_scaled<E>(up, uq, valid, c2, rp.nDp, rp.nDq, rho, r));
                     }
-                    const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
-                    double a0 = b4 ? d[2] : d[0], a1 = b4 ? d[3] : d[1];
-                    a0 = __dadd_rn(a0, __shfl_xor_sync(0xFFFFFFFFu, b4 ? d[0] : d[2], 16));
-                    a1 = __dadd_rn(a1, __shfl_xor_sync(0xFFFFFFFFu, b4 ? d[1] : d[3], 16));
-                    double m = b3 ? a1 : a0;
-                    m = __dadd_rn(m, __shfl_xor_sync(0xFFFFFFFFu, b3 ? a0 : a1, 8));
+                    const bool b4 = (lane >> 4) & 1;
+                    double m;
+                    int gs;
+                    if constexpr (SPW == 4) {
+                        const bool b3 = (lane >> 3) & 1;
+                        double a0 = b4 ? d[2] : d[0], a1 = b4 ? d[3] : d[1];
+                        a0 = __dadd_rn(a0, __shfl_xor_sync(0xFFFFFFFFu, b4 ? d[0] : d[2], 16));
+                        a1 = __dadd_rn(a1, __shfl_xor_sync(0xFFFFFFFFu, b4 ? d[1] : d[3], 16));
+                        m = b3 ? a1 : a0;
+                        m = __dadd_rn(m, __shfl_xor_sync(0xFFFFFFFFu, b3 ? a0 : a1, 8));
 #pragma unroll
-                    for (int o = 4; o > 0; o >>= 1) m = __dadd_rn(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
-                    const int gs = u * USEG + 4 * warp + 2 * b4 + b3;   // this lane group's segment
-                    if ((lane & 7) == 0 && gs < nseg) segm[gs] = m;
+                        for (int o = 4; o > 0; o >>= 1) m = __dadd_rn(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+                        gs = u * USEG + 4 * warp + 2 * b4 + b3;   // this lane group's segment
+                    } else {
+                        m = b4 ? d[1] : d[0];
+                        m = __dadd_rn(m, __shfl_xor_sync(0xFFFFFFFFu, b4 ? d[0] : d[1], 16));
+#pragma unroll
+                        for (int o = 8; o > 0; o >>= 1) m = __dadd_rn(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+                        gs = u * USEG + 2 * warp + b4;
+                    }
+                    if ((lane & (32 / SPW - 1)) == 0 && gs < nseg) segm[gs] = m;
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[sl]);
                 }
             }
             __syncthreads();
+            if (tid == 0 && attempt == 0) SD_TRS(P, 4);
             // ---- block masses (32 segments each; warp tree sums) and the total --------------
             const int nblk = (nseg + 31) / 32;
             for (int bk = warp; bk < nblk; bk += NW) {
@@ -1400,6 +1415,7 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
             __syncthreads();
         }
         // ---- level 3: re-read the found segment, scan it, find the lane and the token -------
+        if (tid == 0) SD_TRS(P, 5);
         if (warp == 0) {
             const int sgsel = s_sel[0];
             const double th2 = s_th;

@@ -4,7 +4,7 @@ sd_debug_trace) -> gpurun_out/rtrace_<cfg>_<dtype>.npz, plus a printed summary.
 k_row_stats record (8 words per CTA, %globaltimer ns): 0 start, 1 after stop-mask read,
 2 p slice arrived, 3 q slice arrived, 4 block reduction done, 5 published (ticket taken),
 6 end, 7 = smid << 32 | flags (1 skipped, 2 last arriver).  k_sample_req: 0 start, 1 after
-griddepcontrol.wait, 2 end.
+griddepcontrol.wait, 2 end, 3 first unit staged, 4 row streamed, 5 block/segment search done.
 Usage on the box: python tools/trace_rowstats.py --config c3
 """
 import argparse
@@ -62,6 +62,12 @@ def summarize(d):
               f"{(S[:, 1].min() - t0) / 1e3:.1f}..{(S[:, 1].max() - t0) / 1e3:.1f}, end "
               f"{(S[:, 2].min() - t0) / 1e3:.1f}..{(S[:, 2].max() - t0) / 1e3:.1f} us; per-CTA "
               f"p50 {np.percentile(S[:, 2] - S[:, 1], 50) / 1e3:.1f} us")
+        ok = (S[:, 3] > 0) & (S[:, 4] > 0) & (S[:, 5] > 0)
+        Q = S[ok]
+        for nm, a_, b_ in (("first unit", 1, 3), ("stream rest", 3, 4), ("block search", 4, 5),
+                           ("level 3 + outputs", 5, 2)):
+            v = (Q[:, b_] - Q[:, a_]) / 1e3
+            print(f"  sampler {nm:18s} p50 {np.percentile(v, 50):5.2f}  p90 {np.percentile(v, 90):5.2f} us")
 
 
 def main():
