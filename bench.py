@@ -5,8 +5,9 @@
 
 A step is one sd_verify call (the whole hot path, rows a1-a10 of SURVEY 8(a)) over one batch of
 synthetic logits that is already resident in HBM.  The default workload is BASELINE.json
-configs[1] (Vicuna-7B shape: V=32000, k=5, B=64, T=1, fp32, kappa=30).  Eight distinct batches
-(720 MB > the 126 MB L2) are rotated so no step reads L2-resident inputs of the previous one.
+configs[2] -- the Llama-3 shape north_star's target is quoted on (V=128256, k=7, B=128 per
+verifier, T=1, fp32, kappa=30).  Eight distinct batches (7.9 GB > the 126 MB L2) are rotated so
+no step reads L2-resident inputs of the previous one.
 K steps are captured in one CUDA graph and timed with CUDA events on the launching stream (a
 second graph of the same K steps with profiling events around k_row_stats gives the roofline's
 kernel time);
@@ -38,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3")
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--temperature", type=float, default=None)
     ap.add_argument("--nbatch", type=int, default=8)
@@ -334,7 +335,7 @@ def run_ours(args):
     # dominant kernel (k_row_stats on the two-launch path; the stream variant's kernel): algorithmic
     # bytes of the whole step per launch / its CUDA-event time on the launching stream
     pl = sd.plan(B, k, V, T, torch.float32 if args.dtype == "f32" else torch.bfloat16)
-    kname = "k_verify_stream" if pl["variant"] == "stream" else "k_row_stats"
+    kname = "k_row_stats"
     kA_mean_ms = statistics.fmean(kA)
     alg_per_launch = alg / K
     peak, peak_kind = load_peaks()
@@ -378,7 +379,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         ems = s0.elapsed_time(s1)
         (ems,), (etok_all,) = reduce_max_sum([ems], [etok], dev)
-        h2d = sum(t.numel() * t.element_size() for t in hb[0].values() if t is not None)
+        h2d = sum(hb[0][x].numel() * hb[0][x].element_size() for x in ("p", "q", "ids")
+                  if hb[0][x] is not None and not (greedy and x == "q"))   # q is not copied at T = 0
         d2h = B * 4 + B * (k + 1) * 4 + B * 4
         e2e = {"value": etok_all / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": E}
@@ -409,7 +411,8 @@ def run_ours(args):
                          "alg_bytes_per_launch": alg_per_launch,
                          "kernel_ms_mean": kA_mean_ms, "kernel_ms_source": kA_src,
                          "kernel_ms_events": statistics.fmean(kA_ev),
-                         "step_gbs": alg_per_launch / (ms_max / K / 1000.0) / 1e9},
+                         "step_gbs": alg_per_launch / (ms_max / K / 1000.0) / 1e9,
+                         "step_frac": alg_per_launch / (ms_max / K / 1000.0) / 1e9 / peak},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": K * pl["launches"],

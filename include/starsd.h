@@ -58,7 +58,10 @@ enum {
     SD_FAULT_NONFINITE = 2,        /* hard: NaN or +inf logit in a reached row               */
     SD_FAULT_EMPTY_ROW = 4,        /* hard: reached row is all -inf                           */
     SD_FAULT_ZERO_Q = 8,           /* info: q_j(x_j) = 0, treated as a rejection at j (C-7)   */
-    SD_FAULT_ZERO_RESIDUAL = 16    /* info: residual mass R == 0, sampled from p_L (C-6)      */
+    SD_FAULT_ZERO_RESIDUAL = 16,   /* info: residual mass R == 0, sampled from p_L (C-6)      */
+    SD_FAULT_PROTOCOL = 32         /* hard: an internal wait of the kernels gave up (200 ms):
+                                      the workspace was used concurrently or corrupted; the
+                                      request's result is void (never set in a correct run)     */
 };
 
 #define SD_MAX_K 31
@@ -99,11 +102,15 @@ typedef struct {
  *   out_tokens    device, [B][k+1] int32: x_0..x_{L-1}, then t, then -1 padding
  *   out_status    device, [B] int32 fault bitmask, or NULL
  *   workspace     device, >= sd_verify_workspace_size() bytes, 16-byte aligned, zero-filled
- *                 once before first use.  Every call leaves the zero region of its shape
- *                 zeroed again (word 0 excepted: a call counter the kernels keep, any value is
- *                 valid), so calls of one shape (batch, k, vocab, dtype, T == 0 or not) reuse it
- *                 as is; before a call of another shape it must be zero-filled again.  One
- *                 workspace must not be used by two calls that may run concurrently.
+ *                 once before its first use.  Every call leaves the zero region of its shape
+ *                 zeroed again (word 0 excepted: a call counter the kernels keep); the library
+ *                 remembers, per workspace pointer in this process, the layout of the last call
+ *                 it enqueued there, and a call of another shape (batch, k, vocab, dtype, T == 0
+ *                 or not) first zero-fills the union of both zero regions on `stream` (a
+ *                 stream-ordered memset).  So one workspace serves any sequence of shapes as long
+ *                 as it is large enough.  One workspace must not be used by two calls that may
+ *                 run concurrently (e.g. on two streams); such misuse is detected by bounded
+ *                 waits inside the kernels and reported as SD_FAULT_PROTOCOL, never as a hang.
  *   stream        CUDA stream the work is ordered on
  * Returns SD_OK (work enqueued), SD_ERR_INVALID_ARGUMENT, or SD_ERR_CUDA (launch failure).
  * The input and output buffers must stay valid until the stream has reached the call.
@@ -118,24 +125,21 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
 sd_status sd_verify_workspace_size(const sd_shape* shape, float temperature, size_t* bytes);
 
 /*
- * sd_verify_plan -- how sd_verify will run this shape on the current device (host only; it
- * may query the device's occupancy limits, but launches nothing).
- *   variant      SD_VARIANT_TWO_LAUNCH (default): k_row_stats (grid = chunk x request x position,
- *                position-major) + k_sample / k_finalize_greedy, PDL-chained;
- *                SD_VARIANT_STREAM (STARSD_KERNEL=stream, when the shape fits): one launch of `ctas`
- *                persistent CTAs in clusters of `cluster`, each streaming a `slice`-logit slice of
- *                every row pair its cluster owns through a TMA ring
+ * sd_verify_plan -- how sd_verify will run this shape (host only; launches nothing).
+ *   variant      SD_VARIANT_TWO_LAUNCH: k_row_stats (grid = chunk x request x position,
+ *                position-major; row statistics, decisions and most sampling chunk tasks) +
+ *                k_sample_tail / k_finalize_greedy, PDL-chained
  *   launches     kernel launches per sd_verify call
- *   cluster, slice, ctas   cluster size (0: none), logits per CTA slice / chunk, CTAs in the first
- *                launch
- *   max_active_clusters, smem_bytes   occupancy of the stream variant (0 otherwise)
+ *   cluster      k_row_stats cluster size (0: none); slice = logits per CTA chunk
+ *   ctas         CTAs of k_row_stats; tail_ctas: CTAs of the second kernel
+ *   tagged       rows publish tagged partials to a start-ticket decider (2..64 chunks per row)
  */
-enum { SD_VARIANT_TWO_LAUNCH = 1, SD_VARIANT_STREAM = 3 };
+enum { SD_VARIANT_TWO_LAUNCH = 1 };
 typedef struct {
     int32_t variant, launches, cluster, slice;
     int64_t ctas;
-    int32_t max_active_clusters;   /* stream variant: clusters the device keeps resident */
-    int32_t smem_bytes;            /* stream variant: dynamic shared memory per CTA       */
+    int64_t tail_ctas;
+    int32_t tagged;
 } sd_plan;
 sd_status sd_verify_plan(const sd_shape* shape, float temperature, sd_plan* out);
 
@@ -152,8 +156,7 @@ sd_status sd_philox_uniforms(uint64_t seed, uint64_t round, const uint32_t* pos,
 /*
  * sd_profile_events -- tracing hook for benchmarks.  After this call, the next n_pairs
  * sd_verify calls on this thread record events[2 i] immediately before and events[2 i + 1]
- * immediately after their dominant kernel (k_row_stats, the HBM-streaming kernel, or the stream
- * variant's single kernel), on the call's
+ * immediately after their dominant kernel (k_row_stats, the HBM-streaming kernel), on the call's
  * stream (graph capture records them as event nodes).  events: host array of 2 * n_pairs
  * caller-created cudaEvent_t handles; n_pairs = 0 disables.  The caller reads the durations
  * with cudaEventElapsedTime.
@@ -173,12 +176,29 @@ sd_status sd_profile_events(cudaEvent_t* events, int32_t n_pairs);
 sd_status sd_profile_timestamps(unsigned long long* device_buf, int32_t n_calls);
 
 /*
- * sd_debug_trace -- development instrumentation of the stream variant (library built with
- * STARSD_BUILD_DEBUG=1; otherwise ignored).  When device_buf != NULL, subsequent stream-variant
- * sd_verify calls on this thread write, per CTA, a record log of kSTraceN = 8192 uint64 words:
- * word 0 = record count, then event records (type << 56 | arg << 40 | %globaltimer), and the
- * last 16 words = clock64 accounting counters (tools/trace_stream.py, tools/analyze_strace.py).
- * NULL disables.
+ * sd_verify_trace -- test/debug hook: the fp64 statistics the most recent sd_verify call on
+ * `workspace` (same shape and temperature > 0, already reached by `stream`) decided with, for the
+ * tolerance checks of north_star ("probabilities and residual masses within 1e-5 relative").
+ * Copied out by a small kernel on `stream` (device pointers):
+ *   accept_len  [B] int32  the out_accept_len that call produced (selects the rows it reached)
+ *   lam_p [B][k+1], lam_q [B][k]   natural-log log-normalisers logsumexp_x z(x)/T of the reached
+ *               rows (j <= L); NaN for rows after L
+ *   a     [B][k]   p_j(x_j)/q_j(x_j) as the acceptance test used it (not clamped to 1; 0 when
+ *               q_j(x_j) = 0); NaN for rows after L or rows with a hard fault
+ *   R     [B]      mass of the distribution the token was sampled from: residual 1 - beta_L
+ *               (P:736), sum p_k at the bonus, sum p_L after the C-6 fallback; NaN if hard
+ * Must be called before the workspace is used again.  Greedy calls have no such statistics
+ * (SD_ERR_INVALID_ARGUMENT).
+ */
+sd_status sd_verify_trace(const sd_shape* shape, float temperature, const void* workspace,
+                          const int32_t* accept_len, double* lam_p, double* lam_q, double* a,
+                          double* R, cudaStream_t stream);
+
+/*
+ * sd_debug_trace -- development instrumentation (library built with STARSD_BUILD_DEBUG=1;
+ * otherwise ignored).  When device_buf != NULL, subsequent sd_verify calls on this thread write
+ * eight uint64 per k_row_stats CTA: %globaltimer at phase points 0..6 and word 7 = smid << 32 |
+ * flags (tools/trace_rowstats.py).  NULL disables.
  */
 sd_status sd_debug_trace(unsigned long long* device_buf);
 
@@ -247,30 +267,43 @@ typedef struct {
 /* Size of the opaque communicator id the caller must broadcast (ncclUniqueId). */
 #define SD_STAR_ID_BYTES 128
 
-/* Draft rank only: generate (world-1) ids, one per (0, v) pair, into ids_out
- * [(world-1) * SD_STAR_ID_BYTES] host bytes.  The caller broadcasts them (e.g. through the
- * torch.distributed store) before every rank calls sd_star_create. */
+/* Draft rank only: generate the communicator ids, two per (0, v) pair -- id 2 (v-1) for the
+ * draft -> verifier direction (ids, q rows), id 2 (v-1) + 1 for the verifier -> draft direction
+ * (accept lengths, tokens) -- into ids_out [2 * (world-1) * SD_STAR_ID_BYTES] host bytes.  The
+ * caller broadcasts them (e.g. through the torch.distributed store) before every rank calls
+ * sd_star_create. */
 sd_status sd_star_unique_ids(int32_t world, void* ids_out);
 
-/* Create the handle: per-pair communicators (blocking, collective over each pair), staging
- * slots sized for max_shape, streams and events. */
+/* Create the handle: per-pair communicators (blocking, collective over each pair; one per
+ * direction, each on its own stream, so a slot's payload ships while another slot's result is in
+ * flight -- the decoupling of P:815-819), staging slots sized for max_shape, streams and events
+ * (including a ring of 1024 pre-created busy-interval event pairs). */
 sd_status sd_star_create(sd_star** out, const sd_star_config* cfg, const void* ids);
 
-/* Draft: enqueue send(ids, q) -> recv(results) for (verifier, slot) on the pair's stream,
- *        ordered after `stream` (where the draft produced ids/q); returns immediately.
- * Verifier: recv(ids, q) into the slot -> sd_verify(p_logits, ...) -> send(results), all
- *        ordered on `stream`; results also land in out_accept_len / out_tokens. */
+/* Draft: enqueue send(ids, q) on the pair's down stream and recv(results) on its up stream for
+ *        (verifier, slot), ordered after `stream` (where the draft produced ids/q); returns at
+ *        once.  The out buffers belong to the library until sd_star_poll returns that slot.
+ * Verifier: recv(ids, q) into the slot's staging (down stream) -> sd_verify(p_logits, ...) on
+ *        `stream` -> send(results) (up stream); results also land in out_accept_len / out_tokens,
+ *        which must stay untouched until sd_star_poll returns the round.  A batch change between
+ *        rounds of a slot is handled (the verify workspace re-zeroes itself). */
 sd_status sd_star_round(sd_star* h, const sd_round_desc* d, cudaStream_t stream);
 
-/* Draft only: pop the next completed return in completion (FIFO) order -- the global request
- * buffer Q_in of Alg. 1.  Waits up to timeout_us (0 = do not wait).  Returns
- * SD_ERR_NOT_READY / SD_ERR_TIMEOUT when nothing completed. */
+/* Draft: pop the next completed return in completion (FIFO) order -- the global request
+ * buffer Q_in of Alg. 1.  Verifier: the oldest round whose results have been sent.
+ * Waits up to timeout_us (0 = do not wait).  Returns SD_ERR_NOT_READY / SD_ERR_TIMEOUT when
+ * nothing completed.  If a round has been in flight for longer than cfg.timeout_ms (> 0), or a
+ * communicator reports an asynchronous error, every communicator of the handle is aborted
+ * (ncclCommAbort) and SD_ERR_TIMEOUT / SD_ERR_NCCL is returned; the handle then only accepts
+ * sd_star_destroy. */
 sd_status sd_star_poll(sd_star* h, int32_t* verifier, int32_t* slot, uint64_t* round,
                        int32_t timeout_us);
 
-/* Draft only: mark the start / end of draft work on `stream` (recorded as CUDA events); the
- * busy fraction is the union of these intervals over the window. */
+/* Draft only: mark the start / end of draft work on `stream` (recorded as CUDA events from a
+ * pre-created ring); the busy fraction is the union of these intervals over the window.
+ * _v tags the interval with the verifier it serves (S(d) per verifier for the analytics). */
 sd_status sd_star_draft_begin(sd_star* h, cudaStream_t stream);
+sd_status sd_star_draft_begin_v(sd_star* h, int32_t verifier, cudaStream_t stream);
 sd_status sd_star_draft_end(sd_star* h, cudaStream_t stream);
 
 sd_status sd_star_stats(sd_star* h, sd_star_stats_t* out);
@@ -285,9 +318,55 @@ sd_status sd_star_destroy(sd_star* h);
  * reports busy fraction, mean idle gap (T_idle, Eq. 9) and mean queueing wait (T_wait).
  * For n_slots = 1 the busy fraction equals N S / (N S + T_idle) with
  * T_idle = max(0, Z - (N - 1) S)  (Eqs. 8-10); the smallest N with no idle gap is ceil(Z/S)+1.
+ * sd_star_simulate_ex: per-verifier service_ms[v-1] / return_ms[v-1] (heterogeneous star, C4);
+ * rounds_out[v-1] (nullable) = services of verifier v counted in the window.
  */
 sd_status sd_star_simulate(int32_t n_verifiers, int32_t n_slots, double service_ms,
                            double return_ms, int32_t rounds, sd_star_stats_t* out);
+sd_status sd_star_simulate_ex(int32_t n_verifiers, int32_t n_slots, const double* service_ms,
+                              const double* return_ms, int32_t rounds, uint64_t* rounds_out,
+                              sd_star_stats_t* out);
+
+/* ======================================================================================
+ * Star analytics and admission (Sec. 4, Eqs. 3-11; N_full / N_max)
+ * ====================================================================================== */
+typedef struct {
+    double expected_accepted;      /* E[l]_gamma = sum_i beta_i (1 - beta_i^d) / (1 - beta_i)   (Eqs. 3-4) */
+    double t_idle_ms;              /* max(0, Z - (N - 1) S)                                      (Eq. 9)    */
+    double t_gamma_ms;             /* N S + T_idle                                               (Eq. 10)   */
+    double throughput_per_ms;      /* O_gamma = E[l]_gamma / T_gamma (accepted tokens per ms)   (Eq. 11)   */
+    double per_target_min_per_ms;  /* min_i E[l_i] / T_gamma                                               */
+    double busy_fraction;          /* N S / T_gamma (the draft's load)                                     */
+    int32_t n_full;                /* ceil(Z / S) + 1: the full-load onset */
+    int32_t n_max;                 /* largest N whose per-target throughput E[l_i]/T_gamma(N) (mean beta)
+                                      stays >= o_alone: the admission bound of P:343-345 (0: none)    */
+    double service_ms, return_ms;  /* the S(d), Z(d) used (online estimates for sd_*_predict)           */
+} sd_star_prediction;
+
+/* Closed forms for n targets with acceptance rates beta[0..n-1], depth d, S(d) = service_ms,
+ * Z(d) = return_ms and a standalone target speed o_alone (tokens per ms). */
+sd_status sd_star_analytics(int32_t n, const double* beta, int32_t d, double service_ms,
+                            double return_ms, double o_alone_per_ms, sd_star_prediction* out);
+
+/* Draft only: feed the accept lengths of a returned round (host copy, n requests) into the online
+ * estimate of verifier v's beta (MLE over the tests evaluated: accepted / (accepted + rejections));
+ * sd_star_predict evaluates the closed forms on the online S(d) (draft busy intervals), Z(d)
+ * (submit -> return, host clock) and betas, and the admission bound N_max. */
+sd_status sd_star_observe(sd_star* h, int32_t verifier, const int32_t* accept_len_host, int32_t n);
+sd_status sd_star_predict(sd_star* h, double o_alone_per_ms, sd_star_prediction* out);
+
+/* Host-only scheduler handle: the star's FIFO scheduler and online estimators for callers that
+ * bring their own transport (e.g. a gloo cross-process star in the tests).  Times are caller ms. */
+typedef struct sd_sched sd_sched;
+sd_status sd_sched_create(sd_sched** out, int32_t n_verifiers, int32_t k);
+sd_status sd_sched_push(sd_sched* h, int32_t verifier, int32_t slot, uint64_t round, double t_ms);
+sd_status sd_sched_pop(sd_sched* h, double now_ms, int32_t* verifier, int32_t* slot, uint64_t* round);
+sd_status sd_sched_service(sd_sched* h, int32_t verifier, double t0_ms, double t1_ms);
+sd_status sd_sched_observe(sd_sched* h, int32_t verifier, double return_ms,
+                           const int32_t* accept_len, int32_t n);
+sd_status sd_sched_stats(sd_sched* h, sd_star_stats_t* out);
+sd_status sd_sched_predict(sd_sched* h, double o_alone_per_ms, sd_star_prediction* out);
+sd_status sd_sched_destroy(sd_sched* h);
 
 /* Static description of a status code. */
 const char* sd_status_string(sd_status s);

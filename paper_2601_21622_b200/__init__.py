@@ -13,11 +13,12 @@ import torch
 from . import _lib
 from ._lib import StarsdError, check
 
-__all__ = ["verify", "verify_host", "workspace_size", "plan", "philox_words", "Workspace", "StarsdError",
-           "version"]
+__all__ = ["verify", "verify_host", "verify_trace", "workspace_size", "plan", "philox_words",
+           "Workspace", "StarsdError", "version"]
 
 FAULT_BAD_DRAFT_ID, FAULT_NONFINITE, FAULT_EMPTY_ROW = 1, 2, 4
-FAULT_ZERO_Q, FAULT_ZERO_RESIDUAL = 8, 16
+FAULT_ZERO_Q, FAULT_ZERO_RESIDUAL, FAULT_PROTOCOL = 8, 16, 32
+HARD_FAULTS = FAULT_BAD_DRAFT_ID | FAULT_NONFINITE | FAULT_EMPTY_ROW | FAULT_PROTOCOL
 
 
 def version() -> str:
@@ -61,26 +62,39 @@ def plan(batch: int, k: int, vocab: int, temperature: float,
           "sd_verify_plan")
     return {"variant": _lib.VARIANT_NAMES.get(out.variant, str(out.variant)),
             "launches": out.launches, "cluster": out.cluster, "slice": out.slice,
-            "ctas": out.ctas, "max_active_clusters": out.max_active_clusters,
-            "smem_bytes": out.smem_bytes}
+            "ctas": out.ctas, "tail_ctas": out.tail_ctas, "tagged": bool(out.tagged)}
 
 
 class Workspace:
-    """A zero-filled device workspace; sd_verify leaves it zero-filled after every call."""
+    """A zero-filled device workspace (zero-filled on `stream`, default: the current stream, so
+    the fill is ordered before the calls that use it there); sd_verify leaves it zero-filled after
+    every call and re-zeroes what it needs when the shape changes (include/starsd.h)."""
 
-    def __init__(self, batch, k, vocab, temperature, dtype=torch.float32, device=None):
+    def __init__(self, batch, k, vocab, temperature, dtype=torch.float32, device=None,
+                 stream: torch.cuda.Stream | None = None):
         self.nbytes = workspace_size(batch, k, vocab, temperature, dtype)
-        self.buf = torch.zeros(max(self.nbytes, 16), dtype=torch.uint8, device=device)
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            self.buf = torch.zeros(max(self.nbytes, 16), dtype=torch.uint8, device=device)
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
 
 
 _ws_cache: dict = {}
 
 
-def _workspace_for(device, batch, k, vocab, temperature, dtype) -> Workspace:
-    key = (str(device), batch, k, vocab, temperature == 0.0, dtype)
+def _workspace_for(device, stream, batch, k, vocab, temperature, dtype) -> Workspace:
+    """One cached workspace per (device, stream, shape): calls on different streams never share
+    one (a workspace must not serve two calls that may run concurrently)."""
+    key = (str(device), stream.cuda_stream, batch, k, vocab, temperature == 0.0, dtype)
     ws = _ws_cache.get(key)
     if ws is None:
-        ws = Workspace(batch, k, vocab, temperature, dtype, device)
+        ws = Workspace(batch, k, vocab, temperature, dtype, device, stream)
         _ws_cache[key] = ws
     return ws
 
@@ -117,9 +131,9 @@ def verify(p: torch.Tensor, q: torch.Tensor | None, ids: torch.Tensor, temperatu
         st = torch.empty(B, dtype=torch.int32, device=p.device)
     else:
         L, tok, st = out
-    ws = workspace or _workspace_for(p.device, B, k, V, float(temperature), p.dtype)
-    sh = _shape(B, k, V, ld_p, ld_q, code)
     s = stream if stream is not None else torch.cuda.current_stream(p.device)
+    ws = workspace or _workspace_for(p.device, s, B, k, V, float(temperature), p.dtype)
+    sh = _shape(B, k, V, ld_p, ld_q, code)
     check(_lib.load().sd_verify(p.data_ptr(), qptr, ids.data_ptr(), ctypes.byref(sh),
                                 float(temperature), seed & (2**64 - 1), round & (2**64 - 1),
                                 request_id_base & (2**64 - 1), L.data_ptr(), tok.data_ptr(),
@@ -136,7 +150,9 @@ def verify_host(p: torch.Tensor, q: torch.Tensor | None, ids: torch.Tensor, temp
     `staging` (optional dict) caches the device buffers between calls."""
     dev = torch.device(device)
     st = staging if staging is not None else {}
-    if "p" not in st or st["p"].shape != p.shape or st["p"].dtype != p.dtype:
+    sig = (tuple(p.shape), p.dtype, None if q is None else (tuple(q.shape), q.dtype), tuple(ids.shape))
+    if st.get("sig") != sig:
+        st["sig"] = sig
         st["p"] = torch.empty(p.shape, dtype=p.dtype, device=dev)
         st["q"] = torch.empty(q.shape, dtype=q.dtype, device=dev) if q is not None else None
         st["ids"] = torch.empty(ids.shape, dtype=torch.int32, device=dev)
@@ -156,6 +172,28 @@ def verify_host(p: torch.Tensor, q: torch.Tensor | None, ids: torch.Tensor, temp
         h.copy_(d, non_blocking=True)
     torch.cuda.current_stream(dev).synchronize()
     return st["host_out"]
+
+
+def verify_trace(p: torch.Tensor, accept_len: torch.Tensor, temperature: float,
+                 workspace: Workspace, vocab: int | None = None, ld_q: int | None = None,
+                 stream: torch.cuda.Stream | None = None) -> dict:
+    """sd_verify_trace: the fp64 statistics the last sampled sd_verify call on `workspace`
+    decided with (lam_p [B, k+1], lam_q [B, k], a [B, k], R [B]; NaN where not reached)."""
+    B, k1, ld_p = p.shape
+    k = k1 - 1
+    V = ld_p if vocab is None else vocab
+    sh = _shape(B, k, V, ld_p, ld_q if ld_q is not None else ld_p, _dtype_code(p))
+    dev = p.device
+    out = {"lam_p": torch.empty(B, k + 1, dtype=torch.float64, device=dev),
+           "lam_q": torch.empty(B, k, dtype=torch.float64, device=dev),
+           "a": torch.empty(B, k, dtype=torch.float64, device=dev),
+           "R": torch.empty(B, dtype=torch.float64, device=dev)}
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    check(_lib.load().sd_verify_trace(ctypes.byref(sh), float(temperature), workspace.buf.data_ptr(),
+                                      accept_len.data_ptr(), out["lam_p"].data_ptr(),
+                                      out["lam_q"].data_ptr(), out["a"].data_ptr(),
+                                      out["R"].data_ptr(), s.cuda_stream), "sd_verify_trace")
+    return out
 
 
 def philox_words(seed: int, round: int, pos: torch.Tensor, rid: torch.Tensor) -> torch.Tensor:

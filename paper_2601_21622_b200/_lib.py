@@ -22,7 +22,10 @@ EXPORTS = ["sd_verify", "sd_verify_workspace_size", "sd_philox_uniforms", "sd_st
            "sd_star_create", "sd_star_round", "sd_star_poll", "sd_star_draft_begin",
            "sd_star_draft_end", "sd_star_stats", "sd_star_destroy", "sd_status_string",
            "sd_last_error", "sd_version", "sd_profile_events", "sd_profile_timestamps", "sd_debug_trace",
-           "sd_star_simulate", "sd_verify_plan"]
+           "sd_star_simulate", "sd_verify_plan", "sd_verify_trace", "sd_star_simulate_ex",
+           "sd_star_analytics", "sd_star_observe", "sd_star_predict", "sd_star_draft_begin_v",
+           "sd_sched_create", "sd_sched_push", "sd_sched_pop", "sd_sched_service",
+           "sd_sched_observe", "sd_sched_stats", "sd_sched_predict", "sd_sched_destroy"]
 
 
 class Shape(ctypes.Structure):
@@ -33,10 +36,10 @@ class Shape(ctypes.Structure):
 class Plan(ctypes.Structure):
     _fields_ = [("variant", ctypes.c_int32), ("launches", ctypes.c_int32),
                 ("cluster", ctypes.c_int32), ("slice", ctypes.c_int32), ("ctas", ctypes.c_int64),
-                ("max_active_clusters", ctypes.c_int32), ("smem_bytes", ctypes.c_int32)]
+                ("tail_ctas", ctypes.c_int64), ("tagged", ctypes.c_int32)]
 
 
-VARIANT_NAMES = {1: "two_launch", 3: "stream"}
+VARIANT_NAMES = {1: "two_launch"}
 
 
 class StarConfig(ctypes.Structure):
@@ -61,6 +64,14 @@ class StarStats(ctypes.Structure):
     _fields_ = [("busy_fraction", ctypes.c_double), ("mean_idle_ms", ctypes.c_double),
                 ("mean_wait_ms", ctypes.c_double), ("window_ms", ctypes.c_double),
                 ("rounds", ctypes.c_uint64)]
+
+
+class Prediction(ctypes.Structure):
+    _fields_ = [("expected_accepted", ctypes.c_double), ("t_idle_ms", ctypes.c_double),
+                ("t_gamma_ms", ctypes.c_double), ("throughput_per_ms", ctypes.c_double),
+                ("per_target_min_per_ms", ctypes.c_double), ("busy_fraction", ctypes.c_double),
+                ("n_full", ctypes.c_int32), ("n_max", ctypes.c_int32),
+                ("service_ms", ctypes.c_double), ("return_ms", ctypes.c_double)]
 
 
 class StarsdError(RuntimeError):
@@ -90,6 +101,8 @@ def load():
     L.sd_verify_workspace_size.restype = st
     L.sd_verify_plan.argtypes = [ctypes.POINTER(Shape), ctypes.c_float, ctypes.POINTER(Plan)]
     L.sd_verify_plan.restype = st
+    L.sd_verify_trace.argtypes = [ctypes.POINTER(Shape), ctypes.c_float, vp, vp, vp, vp, vp, vp, vp]
+    L.sd_verify_trace.restype = st
     L.sd_philox_uniforms.argtypes = [u64, u64, vp, vp, i32, vp, vp]
     L.sd_philox_uniforms.restype = st
     L.sd_star_unique_ids.argtypes = [i32, vp]
@@ -112,6 +125,34 @@ def load():
     L.sd_star_simulate.argtypes = [i32, i32, ctypes.c_double, ctypes.c_double, i32,
                                    ctypes.POINTER(StarStats)]
     L.sd_star_simulate.restype = st
+    dbl = ctypes.c_double
+    pd = ctypes.POINTER(dbl)
+    L.sd_star_simulate_ex.argtypes = [i32, i32, vp, vp, i32, vp, ctypes.POINTER(StarStats)]
+    L.sd_star_simulate_ex.restype = st
+    L.sd_star_analytics.argtypes = [i32, vp, i32, dbl, dbl, dbl, ctypes.POINTER(Prediction)]
+    L.sd_star_analytics.restype = st
+    L.sd_star_observe.argtypes = [vp, i32, vp, i32]
+    L.sd_star_observe.restype = st
+    L.sd_star_predict.argtypes = [vp, dbl, ctypes.POINTER(Prediction)]
+    L.sd_star_predict.restype = st
+    L.sd_star_draft_begin_v.argtypes = [vp, i32, vp]
+    L.sd_star_draft_begin_v.restype = st
+    L.sd_sched_create.argtypes = [ctypes.POINTER(vp), i32, i32]
+    L.sd_sched_create.restype = st
+    L.sd_sched_push.argtypes = [vp, i32, i32, u64, dbl]
+    L.sd_sched_push.restype = st
+    L.sd_sched_pop.argtypes = [vp, dbl, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(u64)]
+    L.sd_sched_pop.restype = st
+    L.sd_sched_service.argtypes = [vp, i32, dbl, dbl]
+    L.sd_sched_service.restype = st
+    L.sd_sched_observe.argtypes = [vp, i32, dbl, vp, i32]
+    L.sd_sched_observe.restype = st
+    L.sd_sched_stats.argtypes = [vp, ctypes.POINTER(StarStats)]
+    L.sd_sched_stats.restype = st
+    L.sd_sched_predict.argtypes = [vp, dbl, ctypes.POINTER(Prediction)]
+    L.sd_sched_predict.restype = st
+    L.sd_sched_destroy.argtypes = [vp]
+    L.sd_sched_destroy.restype = st
     L.sd_profile_events.argtypes = [vp, i32]
     L.sd_profile_events.restype = st
     L.sd_profile_timestamps.argtypes = [vp, i32]

@@ -1,5 +1,5 @@
 // abi.cu -- the extern "C" boundary of libstarsd.so (include/starsd.h): argument validation,
-// workspace layout, dispatch to the sm_100a kernels, status strings.
+// workspace layout and bookkeeping, dispatch to the sm_100a kernels, status strings.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 
 #include "../../include/starsd.h"
 #include "abi_internal.h"
@@ -18,6 +20,8 @@ cudaError_t launch_verify(const Params& P, bool greedy, bool bf16, cudaStream_t 
                           cudaEvent_t ev0, cudaEvent_t ev1);
 cudaError_t launch_philox(uint64_t seed, uint64_t round, const uint32_t* pos, const uint64_t* rid,
                           int n, uint32_t* out, cudaStream_t st);
+cudaError_t launch_trace(const Params& P, const int32_t* accept_len, double* lam_p, double* lam_q,
+                         double* a, double* R, cudaStream_t st);
 
 static thread_local char g_err[512] = "";
 static thread_local cudaEvent_t* g_prof_ev = nullptr;
@@ -36,29 +40,9 @@ sd_status fail(sd_status s, const char* fmt, ...) {
 void clear_error() { g_err[0] = '\0'; }
 const char* last_error() { return g_err; }
 
-// Kernel variant.  Default: the two-launch path (verify_kernels.cu: k_row_stats + k_sample /
-// k_finalize_greedy, PDL-chained), measured fastest on B200 for every BASELINE config.
-// STARSD_KERNEL=stream selects the persistent warp-specialized cluster kernel (verify_stream.cu)
-// when the shape fits it: a cross-variant parity check and design study.
-enum Variant { kTwoLaunch = 1, kStream = 3 };
-static Variant variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("STARSD_KERNEL");
-        v = (e && strcmp(e, "stream") == 0) ? kStream : kTwoLaunch;
-    }
-    return static_cast<Variant>(v);
-}
-
-bool stream_config(int32_t V, int esz, bool greedy, StreamPlan* out);
-cudaError_t launch_stream(const SParams& P, bool greedy, bool bf16, size_t smem, cudaStream_t st,
-                          cudaEvent_t ev0, cudaEvent_t ev1);
-
-void record_event(cudaEvent_t ev, cudaStream_t st);
-
-// The stream kernel uses a prefix of the two-launch layout (rej_mask, ticketB, rowstat).
-static size_t ws_bytes(int32_t B, int32_t k, int32_t V, int32_t esz) {
-    return ws_layout(B, k, V, esz).total;
+static int env_flag(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
 }
 
 constexpr int32_t kMaxVocab = 1 << 24;
@@ -94,6 +78,79 @@ sd_status check_shape(const sd_shape* s, float T, int* esz) {
     return SD_OK;
 }
 
+// ---- workspace bookkeeping --------------------------------------------------------------------
+// Every call leaves the zero region of ITS layout zeroed.  The library remembers, per workspace
+// pointer, the layout of the last call it enqueued there; a call whose layout differs first
+// zero-fills (stream-ordered memset) the union of both zero regions -- past word 0, the call
+// counter the tagged partials derive their tags from, which must keep increasing.  So one
+// workspace serves any sequence of shapes (include/starsd.h).
+struct WsSig {
+    int32_t B, k, V, esz;
+    bool greedy;
+    size_t zero_bytes;
+    bool operator==(const WsSig& o) const {
+        return B == o.B && k == o.k && V == o.V && esz == o.esz && greedy == o.greedy;
+    }
+};
+static std::mutex g_ws_mu;
+static std::unordered_map<uintptr_t, WsSig> g_ws;
+
+static sd_status ws_prepare(void* ws, const WsSig& sig, cudaStream_t st) {
+    size_t clear = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_ws_mu);
+        auto it = g_ws.find(reinterpret_cast<uintptr_t>(ws));
+        if (it == g_ws.end()) {
+            g_ws.emplace(reinterpret_cast<uintptr_t>(ws), sig);   // zero-filled by the caller
+        } else if (!(it->second == sig)) {
+            clear = it->second.zero_bytes > sig.zero_bytes ? it->second.zero_bytes : sig.zero_bytes;
+            it->second = sig;
+        }
+    }
+    if (clear > 16) {
+        const cudaError_t e = cudaMemsetAsync(static_cast<char*>(ws) + 16, 0, clear - 16, st);
+        if (e != cudaSuccess)
+            return fail(SD_ERR_CUDA, "workspace reset: %s", cudaGetErrorString(e));
+    }
+    return SD_OK;
+}
+
+// Shared by sd_verify and sd_verify_trace: the kernels' view of a call.
+static void fill_params(Params& P, const sd_shape* shape, int esz, float temperature,
+                        void* workspace) {
+    const bool greedy = temperature == 0.0f;
+    const WsLayout w = ws_layout(shape->batch, shape->k, shape->vocab, esz);
+    char* ws = static_cast<char*>(workspace);
+    P.B = shape->batch;
+    P.k = shape->k;
+    P.V = shape->vocab;
+    P.ld_p = shape->ld_p ? shape->ld_p : shape->vocab;
+    P.ld_q = shape->ld_q ? shape->ld_q : shape->vocab;
+    chunking(P.V, esz, &P.nch, &P.CH);
+    P.CL = row_cluster(P.nch);
+    P.G = (P.nch + P.CL - 1) / P.CL;
+    P.nseg = P.CH / (32 * (kVecBytes / esz));
+    // c2 = log2(e) / T rounded to fp32; every exponent in the kernels uses this one constant
+    P.c2 = greedy ? 0.0f : static_cast<float>(1.4426950408889634 / static_cast<double>(temperature));
+    P.c2d = static_cast<double>(P.c2);
+    P.epoch = reinterpret_cast<uint32_t*>(ws + w.epoch);
+    P.state = reinterpret_cast<unsigned long long*>(ws + w.state);
+    P.ticketA = reinterpret_cast<uint32_t*>(ws + w.ticketA);
+    P.ticketB = reinterpret_cast<uint32_t*>(ws + w.ticketB);
+    P.tailT = reinterpret_cast<uint32_t*>(ws + w.tailT);
+    P.rowstat = reinterpret_cast<RowStat*>(ws + w.rowstat);
+    P.partA = reinterpret_cast<PartA*>(ws + w.partA);
+    P.partB = reinterpret_cast<PartB*>(ws + w.partB);
+    P.segtab = reinterpret_cast<double2*>(ws + w.segtab);
+    P.rres = reinterpret_cast<double*>(ws + w.rres);
+    P.partT = reinterpret_cast<unsigned long long*>(ws + w.partT);
+    static const int tag = env_flag("STARSD_PUBLISH_TICKET", 0) ? 0 : 1;   // A/B knob
+    P.tagpub = (tag && P.CL == 1 && P.nch >= 2 && P.nch <= kMaxTagNch) ? 1 : 0;
+    static const int chain = env_flag("STARSD_CHAIN", 1);   // 0: plain stream order
+    P.chain = chain ? 1 : 0;
+    P.esz = esz;
+}
+
 }  // namespace sd
 
 using namespace sd;
@@ -106,7 +163,7 @@ sd_status sd_verify_workspace_size(const sd_shape* shape, float temperature, siz
     sd_status s = check_shape(shape, temperature, &esz);
     if (s != SD_OK) return s;
     if (!bytes) return fail(SD_ERR_INVALID_ARGUMENT, "bytes is NULL");
-    *bytes = ws_bytes(shape->batch, shape->k, shape->vocab, esz);
+    *bytes = ws_layout(shape->batch, shape->k, shape->vocab, esz).total;
     return SD_OK;
 }
 
@@ -129,111 +186,53 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     if (!workspace) return fail(SD_ERR_INVALID_ARGUMENT, "workspace is NULL");
     if (!aligned16(p_logits) || (!greedy && !aligned16(q_logits)) || !aligned16(workspace))
         return fail(SD_ERR_INVALID_ARGUMENT, "p_logits / q_logits / workspace not 16-byte aligned");
-    const size_t need = ws_bytes(shape->batch, shape->k, shape->vocab, esz);
-    if (workspace_bytes < need)
+    const WsLayout w = ws_layout(shape->batch, shape->k, shape->vocab, esz);
+    if (workspace_bytes < w.total)
         return fail(SD_ERR_INVALID_ARGUMENT, "workspace_bytes=%zu < required %zu",
-                    workspace_bytes, need);
+                    workspace_bytes, w.total);
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (g_prof_ev && g_prof_i < g_prof_n) {
         ev0 = g_prof_ev[2 * g_prof_i];
         ev1 = g_prof_ev[2 * g_prof_i + 1];
         ++g_prof_i;
     }
-    // c2 = log2(e) / T rounded to fp32; every exponent in the kernels uses this one constant
-    const float c2 =
-        greedy ? 0.0f : static_cast<float>(1.4426950408889634 / static_cast<double>(temperature));
-    const WsLayout w = ws_layout(shape->batch, shape->k, shape->vocab, esz);
-    char* ws = static_cast<char*>(workspace);
-    StreamPlan sp;
-    if (variant() == kStream && stream_config(shape->vocab, esz, greedy, &sp)) {
-        SParams S{};
-        S.p = p_logits;
-        S.q = greedy ? nullptr : q_logits;
-        S.ids = draft_ids;
-        S.B = shape->batch;
-        S.k = shape->k;
-        S.V = shape->vocab;
-        S.ld_p = shape->ld_p ? shape->ld_p : shape->vocab;
-        S.ld_q = shape->ld_q ? shape->ld_q : shape->vocab;
-        S.C = sp.C;
-        S.G = sp.G;
-        S.W = sp.W;
-        S.segmax = sp.segmax;
-        S.nslot = sp.nslot;
-        S.c2 = c2;
-        S.seed = seed;
-        S.round = round;
-        S.rid_base = request_id_base;
-        S.out_L = out_accept_len;
-        S.out_tok = out_tokens;
-        S.out_status = out_status;
-        S.rej_mask = reinterpret_cast<uint32_t*>(ws + w.rej_mask);
-        S.ticket = reinterpret_cast<uint32_t*>(ws + w.ticketB);
-        S.rowres = reinterpret_cast<int2*>(ws + w.rowstat);
-        S.trace = g_trace;
-        {
-            static int dbg = -1;
-            if (dbg < 0) {
-                const char* e = getenv("STARSD_DEBUG");
-                dbg = e ? atoi(e) : 0;
-            }
-            S.debug = dbg;
-        }
-        cudaError_t e = launch_stream(S, greedy, shape->dtype == SD_DTYPE_BF16, sp.smem, stream, ev0, ev1);
-        if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
-        return SD_OK;
-    }
+    s = ws_prepare(workspace, WsSig{shape->batch, shape->k, shape->vocab, esz, greedy, w.zero_bytes},
+                   stream);
+    if (s != SD_OK) return s;
     Params P{};
+    fill_params(P, shape, esz, temperature, workspace);
     P.p = p_logits;
     P.q = greedy ? nullptr : q_logits;
     P.ids = draft_ids;
-    P.B = shape->batch;
-    P.k = shape->k;
-    P.V = shape->vocab;
-    P.ld_p = shape->ld_p ? shape->ld_p : shape->vocab;
-    P.ld_q = shape->ld_q ? shape->ld_q : shape->vocab;
-    chunking(P.V, esz, &P.nch, &P.CH);
-    P.CL = row_cluster(P.nch);
-    P.G = (P.nch + P.CL - 1) / P.CL;
-    P.nseg = P.CH / (32 * (kVecBytes / esz));
-    P.c2 = c2;
-    P.c2d = static_cast<double>(P.c2);
     P.seed = seed;
     P.round = round;
     P.rid_base = request_id_base;
     P.out_L = out_accept_len;
-    P.trace = g_trace;
-    P.prof_ts = nullptr;
-    P.epoch = reinterpret_cast<uint32_t*>(ws + w.epoch);
-    P.partT = reinterpret_cast<unsigned long long*>(ws + w.partT);
-    {
-        static int tag = -1;   // STARSD_PUBLISH=ticket: release-ordered partials + row ticket
-        if (tag < 0) {
-            const char* e = getenv("STARSD_PUBLISH");
-            tag = (e && strcmp(e, "ticket") == 0) ? 0 : 1;
-        }
-        P.tagpub = (tag && P.CL == 1 && P.nch >= 2 && P.nch <= kMaxTagNch) ? 1 : 0;
-    }
-    if (g_ts && g_ts_i < g_ts_n) P.prof_ts = g_ts + 2 * static_cast<size_t>(g_ts_i++);
-    {
-        static int chain = -1;   // STARSD_CHAIN=0: plain stream order before k_row_stats
-        if (chain < 0) {
-            const char* e = getenv("STARSD_CHAIN");
-            chain = (e && strcmp(e, "0") == 0) ? 0 : 1;
-        }
-        P.chain = chain;
-    }
     P.out_tok = out_tokens;
     P.out_status = out_status;
-    P.rej_mask = reinterpret_cast<uint32_t*>(ws + w.rej_mask);
-    P.ticketA = reinterpret_cast<uint32_t*>(ws + w.ticketA);
-    P.ticketB = reinterpret_cast<uint32_t*>(ws + w.ticketB);
-    P.rowstat = reinterpret_cast<RowStat*>(ws + w.rowstat);
-    P.partA = reinterpret_cast<PartA*>(ws + w.partA);
-    P.partB = reinterpret_cast<PartB*>(ws + w.partB);
-    P.segtab = reinterpret_cast<double2*>(ws + w.segtab);
-
+    P.trace = g_trace;
+    P.prof_ts = nullptr;
+    if (g_ts && g_ts_i < g_ts_n) P.prof_ts = g_ts + 2 * static_cast<size_t>(g_ts_i++);
     cudaError_t e = launch_verify(P, greedy, shape->dtype == SD_DTYPE_BF16, stream, ev0, ev1);
+    if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return SD_OK;
+}
+
+sd_status sd_verify_trace(const sd_shape* shape, float temperature, const void* workspace,
+                          const int32_t* accept_len, double* lam_p, double* lam_q, double* a,
+                          double* R, cudaStream_t stream) {
+    clear_error();
+    int esz;
+    sd_status s = check_shape(shape, temperature, &esz);
+    if (s != SD_OK) return s;
+    if (temperature == 0.0f)
+        return fail(SD_ERR_INVALID_ARGUMENT, "sd_verify_trace: sampled calls only (T > 0)");
+    if (shape->batch == 0) return SD_OK;
+    if (!workspace || !accept_len || !lam_p || !lam_q || !a || !R)
+        return fail(SD_ERR_INVALID_ARGUMENT, "sd_verify_trace: NULL argument");
+    Params P{};
+    fill_params(P, shape, esz, temperature, const_cast<void*>(workspace));
+    cudaError_t e = launch_trace(P, accept_len, lam_p, lam_q, a, R, stream);
     if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
     return SD_OK;
 }
@@ -244,19 +243,7 @@ sd_status sd_verify_plan(const sd_shape* shape, float temperature, sd_plan* out)
     sd_status s = check_shape(shape, temperature, &esz);
     if (s != SD_OK) return s;
     if (!out) return fail(SD_ERR_INVALID_ARGUMENT, "out is NULL");
-    const bool greedy = temperature == 0.0f;
     *out = sd_plan{};
-    StreamPlan sp;
-    if (variant() == kStream && stream_config(shape->vocab, esz, greedy, &sp)) {
-        out->variant = SD_VARIANT_STREAM;
-        out->launches = 1;
-        out->cluster = sp.C;
-        out->slice = sp.W;
-        out->ctas = (int64_t)sp.G * sp.C;
-        out->max_active_clusters = sp.G;
-        out->smem_bytes = (int32_t)sp.smem;
-        return SD_OK;
-    }
     int32_t nch, CH;
     chunking(shape->vocab, esz, &nch, &CH);
     out->variant = SD_VARIANT_TWO_LAUNCH;
@@ -265,6 +252,11 @@ sd_status sd_verify_plan(const sd_shape* shape, float temperature, sd_plan* out)
     const int32_t CL = row_cluster(nch), G = (nch + CL - 1) / CL;
     out->cluster = CL > 1 ? CL : 0;
     out->ctas = (int64_t)(shape->k + 1) * shape->batch * (CL > 1 ? G * CL : nch);
+    const int32_t nseg_row = (shape->vocab + 32 * (16 / esz) - 1) / (32 * (16 / esz));
+    out->tail_ctas = temperature == 0.0f ? (shape->batch + 127) / 128
+                     : nseg_row <= 2048   ? shape->batch                       /* k_sample_req */
+                                          : (int64_t)nch * shape->batch;       /* k_sample_chunked */
+    out->tagged = (CL == 1 && nch >= 2 && nch <= kMaxTagNch && !env_flag("STARSD_PUBLISH_TICKET", 0));
     return SD_OK;
 }
 
@@ -322,6 +314,6 @@ const char* sd_status_string(sd_status s) {
 
 const char* sd_last_error(void) { return last_error(); }
 
-const char* sd_version(void) { return "starsd-b200 0.1 (sm_100a)"; }
+const char* sd_version(void) { return "starsd-b200 0.2 (sm_100a)"; }
 
 }  // extern "C"

@@ -15,6 +15,11 @@ constexpr int kMaxChunkBytes = 16 * 1024;          // one CTA owns <= 16 KB of a
 constexpr int kRowClusterDefault = 8;              // see row_cluster()
 constexpr int kMaxTagNch = 64;                     // tagged partials: rows of at most 64 chunks
 
+// status bits (values of include/starsd.h SD_FAULT_*)
+constexpr int32_t kBadId = 1, kNonfinite = 2, kEmptyRow = 4, kZeroQ = 8, kZeroResidual = 16,
+                  kProtocol = 32;
+constexpr int32_t kHard = kBadId | kNonfinite | kEmptyRow | kProtocol;
+
 // Per (request b, position j, vocab chunk c): what one kernel-A CTA found in its slice.
 struct PartA {
     double S_p, S_q;     // sum over the slice of 2^(z c2 - D_c), c2 = log2(e)/T (fp64 across threads)
@@ -25,10 +30,12 @@ struct PartA {
 };
 constexpr int32_t kPartNonfiniteP = 1, kPartNonfiniteQ = 2, kPartHasX = 4, kPartSkipped = 8;
 
-// Per (request b, position j): the whole-row statistics, written by the last kernel-A CTA of
-// that row pair, read by the sampling kernel.
+// Per (request b, position j): the whole-row statistics, written by the CTA that decides the row,
+// read by the sampler and by sd_verify_trace.
 struct RowStat {
     double S_p, S_q;     // row sums of 2^(z c2 - D) (same scale as PartA)
+    double a;            // p_j(x_j) / q_j(x_j) as the decision used it (not clamped to 1); NaN if
+                         // no test was evaluated (bonus row, faults, q_j(x_j) = 0)
     float M_p, M_q;      // sampled: scaled row maxima D = max fl(z_max c2); greedy: raw max of p
     int32_t status;      // SD_FAULT_* bits decided at this position
     int32_t argmax;      // greedy: argmax of p row (lowest index)
@@ -58,25 +65,32 @@ struct Params {
     int32_t* out_tok;
     int32_t* out_status;
     // workspace (zero-filled region first)
-    uint32_t* rej_mask;          // [B]    bit j: position j rejected or faulted
-    uint32_t* ticketA;           // [B][k+1]
-    uint32_t* ticketB;           // [B]
+    unsigned long long* state;   // [B]  bits 0..k: position decided; bits 32+j: position j stopped
+                                 //      the chain (rejection or fault).  The request is settled at
+                                 //      L once positions 0..L are decided and L is the lowest stop
+                                 //      (or L = k with no stop)
+    uint32_t* ticketA;           // [B][k+1] row tickets (tagged rows: start order; else arrival)
+    uint32_t* ticketB;           // [B]    sampling chunk tasks finished
+    uint32_t* tailT;             // [B]    k_sample_chunked CTAs finished
     RowStat* rowstat;            // [B][k+1]
     PartA* partA;                // [B][k+1][nch]
     PartB* partB;                // [B][nch]
     double2* segtab;             // [B][nch][nseg]  (r mass, p mass) per warp segment
+    double* rres;                // [B] mass R of the sampling distribution (trace)
     int32_t nseg;                // segments per chunk
     unsigned long long* trace;   // debug builds only (SD_STREAM_DEBUG): per-CTA phase timestamps
     unsigned long long* prof_ts; // sd_profile_timestamps: [2] this call's span words, or NULL
     // tagged partials (tagpub, rows of 2..kMaxTagNch chunks without clusters): every word of a
     // chunk partial carries the call's tag, so a CTA publishes with plain stores and exits; the
-    // row's last chunk CTA polls the words of the others and decides (no fence, no ticket)
+    // row's decider -- the CTA that took the row's last start ticket -- polls the words of the
+    // others and decides (no fence; it only waits on CTAs that started before it)
     int32_t tagpub;
     uint32_t* epoch;             // [1]  workspace word 0: calls completed on this workspace
                                  //      (tag = (epoch + 1) | 2^31, never a small integer)
     unsigned long long* partT;   // [B][k+1][nch][5 * 2]  tag << 32 | 32 data bits
     int32_t chain;               // k_row_stats launched as a programmatic dependent of whatever
                                  // kernel precedes it on the stream (griddepcontrol.wait first)
+    int32_t esz;                 // bytes per logit
 };
 
 // k_row_stats cluster size for a row of nch chunks: a cluster covers the whole row when nch <= 8
@@ -103,10 +117,10 @@ inline int32_t row_cluster(int32_t nch) {
 }
 
 // Workspace layout for a shape; all offsets 16-byte aligned.  The first `zero_bytes` must be
-// zero before a call and are zero again after it.
+// zero before a call and are zero again after it (word 0, the call counter, excepted).
 struct WsLayout {
-    size_t rej_mask, ticketA, ticketB, epoch, zero_bytes;
-    size_t rowstat, partA, partB, segtab, partT, total;
+    size_t epoch, state, ticketA, ticketB, tailT, zero_bytes;
+    size_t rowstat, partA, partB, segtab, rres, partT, total;
 };
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -128,61 +142,20 @@ inline WsLayout ws_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
     WsLayout w{};
     size_t o = 0;
     w.epoch = o;    o = align16(o + sizeof(uint32_t));   // fixed offset 0 for every shape
-    w.rej_mask = o; o = align16(o + sizeof(uint32_t) * B);
+    w.state = o;    o = align16(o + sizeof(unsigned long long) * B);
     w.ticketA = o;  o = align16(o + sizeof(uint32_t) * (size_t)B * (k + 1));
     w.ticketB = o;  o = align16(o + sizeof(uint32_t) * B);
+    w.tailT = o;    o = align16(o + sizeof(uint32_t) * B);
     w.zero_bytes = o;
     w.rowstat = o;  o = align16(o + sizeof(RowStat) * (size_t)B * (k + 1));
     w.partA = o;    o = align16(o + sizeof(PartA) * (size_t)B * (k + 1) * nch);
     w.partB = o;    o = align16(o + sizeof(PartB) * (size_t)B * nch);
     w.segtab = o;   o = align16(o + sizeof(double) * 2 * (size_t)B * nch * nseg);
+    w.rres = o;     o = align16(o + sizeof(double) * (size_t)B);
     w.partT = o;
     if (nch >= 2 && nch <= kMaxTagNch) o = align16(o + 80 * (size_t)B * (k + 1) * nch);
     w.total = o;
     return w;
 }
-
-// ---- stream kernel (opt-in): persistent warp-specialized clusters --------------------------------
-constexpr int kSStatsWarps = 8;
-constexpr int kSRowWarps = 4;
-constexpr int kSProducers = 2;             // producer lanes issuing main-ring copies (tools/tma_probe:
-                                           // 2 threads x 32 KB copies saturate HBM)
-constexpr int kSThreads = 32 * (1 + kSStatsWarps + kSRowWarps + 1);   // + main / residual producers
-constexpr uint32_t kSPieceBytes = 32768;   // ring slot = one 32 KB bulk copy (tools/tma_probe:
-                                           // one issuing thread sustains ~49 GB/s/SM with 32 KB
-                                           // copies, ~25 GB/s/SM with 16 KB)
-constexpr int kSMaxSlots = 16;
-constexpr int kSResSlots = 2;              // residual re-read ring (one p/q piece pair)
-
-struct SParams {
-    const void* p;
-    const void* q;
-    const int32_t* ids;
-    int32_t B, k, V;
-    int64_t ld_p, ld_q;          // elements
-    int32_t C, G;                // CTAs per cluster, persistent clusters
-    int32_t W;                   // vocabulary slice per CTA (elements, multiple of 16 bytes)
-    int32_t segmax;              // residual segments per slice (table stride)
-    int32_t nslot;               // ring slots
-    float c2;                    // log2(e) / T in fp32 (0 for greedy)
-    uint64_t seed, round, rid_base;
-    int32_t* out_L;
-    int32_t* out_tok;
-    int32_t* out_status;
-    uint32_t* rej_mask;          // [B] bit j: position j stopped the chain (zero region)
-    uint32_t* ticket;            // [B] rows of the request finished (zero region)
-    int2* rowres;                // [B][k+1] (token, status) of a stopping / bonus row
-    unsigned long long* trace;   // development event log (nullptr in production), see below
-    int32_t debug;               // development knobs (0 in production): bit0 stats warps skip the
-                                 // arithmetic (bandwidth probe; results are wrong)
-};
-// trace layout: [grid][kSTraceN] records ((type << 56) | (arg << 40) | (globaltimer & 2^40-1));
-// record 0 of a CTA holds the number of records it wrote.
-constexpr int kSTraceN = 8192;
-
-struct StreamPlan {
-    int32_t C, G, W, segmax, nslot;
-    size_t smem;
-};
 
 }  // namespace sd

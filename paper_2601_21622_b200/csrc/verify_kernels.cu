@@ -4,20 +4,27 @@
 //   accept x_j iff u_acc(j) < min(1, p_j(x_j) / q_j(x_j)),  L = first rejection (else k),
 //   emit x_0..x_{L-1} and t ~ norm(max(0, p_L - q_L)) (L < k) or t ~ p_k (L == k).
 //
-// Data flow (two launches, stream ordered):
-//   k_row_stats  grid = (k+1) * B * nch CTAs in POSITION-MAJOR order (all requests' position 0
-//                first).  CTA (j, b, c) TMA-bulk-loads its 32 KB vocab slice of p_j (and q_j)
-//                into shared memory, computes the slice max and sum of 2^((z - M) log2e / T)
-//                (one MUFU.EX2 per element, fp64 accumulation), and gathers z(x_j).  The last
-//                CTA of a row pair combines the slices (fp64), draws u_acc from Philox and
-//                decides the acceptance test; a rejection sets bit j of rej_mask[b].
-//                A CTA whose request already has a rejection at an earlier position skips its
-//                loads: the method never needs rows after L (laziness).
-//   k_sample     grid = B * nch.  CTA (b, c) re-reads slice c of row L (usually from L2),
-//                computes r = max(0, p - q) in fp64 and per-warp-segment masses; the last CTA
-//                of the request does the inverse-CDF search chunk -> segment -> token.
-//   greedy (T = 0) replaces the sum by an (max, lowest index) reduction and k_sample by a tiny
-//                finalize kernel.
+// Data flow (two launches, stream ordered, PDL-chained):
+//   k_row_stats   grid = (chunk c, request b, position j), POSITION-MAJOR (all requests' position
+//                 0 first).  CTA (c, b, j) TMA-bulk-loads its 16 KB slice of p_j (and q_j), computes
+//                 the slice max and sum of 2^((z - M) log2e / T) (one MUFU.EX2 per element, fp64
+//                 across threads) and gathers z(x_j).  The row's partials meet in one CTA (cluster
+//                 leader / start-order decider / last ticket), which draws u_acc from Philox,
+//                 decides the acceptance test and ORs "decided" (and "stopped") bits into the
+//                 request's 64-bit state word.
+//                 A CTA whose request already stopped below j skips its load (laziness, SURVEY
+//                 8(d)).  If the request is SETTLED at L = j - 1 (positions 0..L decided, L the
+//                 first stop), that CTA instead runs sampling chunk task c of row L: it re-reads
+//                 chunk c of (p_L, q_L) -- read one position wave earlier, so from L2 --, computes
+//                 r = max(0, p - q) per 32-vector segment (fp64 masses) and publishes them; the
+//                 request's last chunk task runs the inverse-CDF search chunk -> segment -> token
+//                 and writes the outputs.
+//   k_sample_req  one CTA per request streams its stop row pair (p_L, q_L) -- or p_k for the
+//                 bonus -- through a TMA ring, computes the residual segment masses on chip and
+//                 runs the inverse-CDF search (k_sample_chunked for vocabularies beyond its
+//                 on-chip table).
+//   greedy (T = 0) replaces the sum by an (max, lowest index) reduction and the tail by a tiny
+//                 finalize kernel.
 // No tensor cores: the step is a streaming reduction, not a contraction.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -26,34 +33,55 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <atomic>
 #include <cstdio>
 
 #include "philox.cuh"
 #include "ptx.cuh"
 #include "verify.cuh"
 
-// Spin-wait.  Debug builds (SD_STREAM_DEBUG) bound it and report the site, so a protocol bug
-// shows up as a message instead of a hung GPU.
-#if SD_STREAM_DEBUG
-#define SD_SPIN(cond, code)                                                                     \
-    for (unsigned long long sd_spin_n = 0; !(cond);)                                            \
-        if (++sd_spin_n == (1ull << 24)) {                                                      \
-            printf("SD_SPIN site %d block (%d,%d,%d) thread %d\n", (code), blockIdx.x, blockIdx.y, \
-                   blockIdx.z, threadIdx.x);                                                    \
-            break;                                                                              \
-        }
-#else
-#define SD_SPIN(cond, code) \
-    while (!(cond)) {       \
-    }
-#endif
-
 namespace sd {
 
-// status bits (values of include/starsd.h SD_FAULT_*)
-constexpr int32_t kBadId = 1, kNonfinite = 2, kEmptyRow = 4, kZeroQ = 8, kZeroResidual = 16;
-constexpr int32_t kHard = kBadId | kNonfinite | kEmptyRow;
 constexpr int kGridY = 32768;   // requests per grid.y span (gridDim.y <= 65535)
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Bounded spin-wait.  Every wait of the protocol is on a CTA that has already started (cluster
+// peers are co-scheduled; a tagged-row decider waits only on CTAs that took a start ticket before
+// it), so a legitimate wait lasts microseconds.  A breach of the workspace contract must not hang
+// the GPU: after kSpinNs the wait gives up and the caller marks the request SD_FAULT_PROTOCOL.
+// Debug builds (SD_STREAM_DEBUG) also print the site.
+constexpr unsigned long long kSpinNs = 200ull * 1000 * 1000;   // 200 ms
+template <typename F>
+__device__ __forceinline__ bool spin_until(F cond, int site) {
+    if (cond()) return true;
+    const unsigned long long t0 = gtimer();
+    for (uint32_t n = 1;; ++n) {
+        if (cond()) return true;
+        if ((n & 255u) == 0u && gtimer() - t0 > kSpinNs) {
+#if SD_STREAM_DEBUG
+            printf("spin_until timeout: site %d block (%d,%d,%d) thread %d\n", site, blockIdx.x,
+                   blockIdx.y, blockIdx.z, threadIdx.x);
+#else
+            (void)site;
+#endif
+            return false;
+        }
+    }
+}
+
+// The accept length of a settled request, else -1: positions 0..L decided and L the lowest stop
+// bit (L = k with no stop).  state: bits 0..31 decided, bits 32..63 stopped.
+__device__ __forceinline__ int settled_L(unsigned long long s, int k) {
+    const uint32_t stop = static_cast<uint32_t>(s >> 32), dec = static_cast<uint32_t>(s);
+    const int L = stop ? __ffs(stop) - 1 : k;
+    const uint32_t need = (2u << L) - 1u;   // bits 0..L (L = 31: all ones)
+    return (dec & need) == need ? L : -1;
+}
 
 // ------------------------------------------------------------------------------------------
 // element types: one 16-byte vector holds 4 fp32 or 8 bf16 logits
@@ -146,15 +174,6 @@ __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
     return v;
 }
 
-// Probability terms of the sampling pass.  Written with explicit-rounding intrinsics so the
-// main pass and the final re-read compute bit-identical values.
-//   p(x) = 2^(z_p c2 - D_p) / S_p ,  r(x) = max(0, p(x) - q(x))   (fp64 after the exp)
-// D is the row's scaled maximum (the largest fl(z_max c2) of the stats pass), S the sum of
-// 2^(z c2 - D) over the row.
-__device__ __forceinline__ double prob_term(float z, float D, float c2, double invS) {
-    return __dmul_rn(static_cast<double>(ex2_approx(__fmaf_rn(z, c2, -D))), invS);
-}
-
 // ---- lean arithmetic of the stats pass (FMNMX3, FFMA2, MUFU.EX2, FADD2) ----------------------
 __device__ __forceinline__ float max3nan(float a, float b, float c) {
     float d;
@@ -232,9 +251,22 @@ __device__ __forceinline__ void thread_stats(const float (&v)[NV][VEC], float c2
 
 // ---- sd_profile_timestamps: fold %globaltimer into a span word (atomic min, no return) -------
 __device__ __forceinline__ void prof_min(unsigned long long* w) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long t = gtimer();
     asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(w), "l"(t) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void state_or_release(unsigned long long* p, unsigned long long bits) {
+    asm volatile("red.release.gpu.global.or.b64 [%0], %1;" ::"l"(p), "l"(bits) : "memory");
+}
+__device__ __forceinline__ uint32_t ticket_relaxed(uint32_t* p) {
+    uint32_t t;
+    asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(p) : "memory");
+    return t;
 }
 
 // ---- outputs --------------------------------------------------------------------------------
@@ -254,12 +286,13 @@ __device__ __forceinline__ void write_outputs(const Params& P, int b, int L, int
 
 // Combination of n slice partials (fp64, exact 2^(D_c - D) rescales); warp-collective, the
 // result is valid in every lane.  SHARED: the partials sit in this CTA's shared memory (cluster
-// leader), else in global memory written by other CTAs of this launch.
+// leader, tagged decider), else in global memory written by other CTAs of this launch.
 struct Comb {
     float RMp, RMq, zxp, zxq;
     double RSp, RSq;
     int flags, RG;
 };
+constexpr int32_t kPartProtocol = 16;   // a wait for this row's partials timed out
 
 template <bool GREEDY, bool SHARED>
 __device__ __forceinline__ Comb combine_parts(const PartA* parts, int n, int lane) {
@@ -334,7 +367,9 @@ __device__ __forceinline__ PartA comb_as_part(const Comb& C) {
     return a;
 }
 
-// The acceptance decision of row pair (b, j) from its whole-row statistics (one thread).
+// The acceptance decision of row pair (b, j) from its whole-row statistics (one thread): the
+// row statistics go to rowstat, then "decided" (and "stopped") bits are ORed into the request's
+// state with release semantics, so a CTA that sees the request settled also sees its rowstat.
 template <bool GREEDY>
 __device__ __forceinline__ void decide(const Params& P, int b, int j, int x, const Comb& C) {
     const int kk = P.k;
@@ -342,7 +377,9 @@ __device__ __forceinline__ void decide(const Params& P, int b, int j, int x, con
     const bool load_q = !GREEDY && j < kk;
     int32_t st = 0;
     bool stop = false;
-    if (j < kk && (x < 0 || x >= P.V)) st = kBadId;
+    double a = NAN;
+    if (C.flags & kPartProtocol) st = kProtocol;
+    if (!st && j < kk && (x < 0 || x >= P.V)) st = kBadId;
     if (!st) {
         if (C.flags & kPartNonfiniteP) st = kNonfinite;
         else if (C.RMp == -INFINITY) st = kEmptyRow;
@@ -359,11 +396,12 @@ __device__ __forceinline__ void decide(const Params& P, int b, int j, int x, con
         } else if (C.zxq == -INFINITY) {
             st = kZeroQ;                                            // q_j(x_j) = 0 (C-7)
             stop = true;
+            a = 0.0;
         } else {
             // a = p(x)/q(x) = 2^((z_p(x) c2 - D_p) - (z_q(x) c2 - D_q)) * S_q / S_p
             const double l = (static_cast<double>(C.zxp) * P.c2d - static_cast<double>(C.RMp)) -
                              (static_cast<double>(C.zxq) * P.c2d - static_cast<double>(C.RMq));
-            const double a = exp2(l) * (C.RSq / C.RSp);
+            a = exp2(l) * (C.RSq / C.RSp);
             if (!(a >= 1.0)) {                                      // a = min(1, p/q) < 1
                 const uint4 w = verify_words(P.seed, static_cast<uint32_t>(j), P.round,
                                              P.rid_base + static_cast<uint64_t>(b));
@@ -374,12 +412,15 @@ __device__ __forceinline__ void decide(const Params& P, int b, int j, int x, con
     RowStat rs;
     rs.S_p = C.RSp;
     rs.S_q = C.RSq;
+    rs.a = a;
     rs.M_p = C.RMp;
     rs.M_q = C.RMq;
     rs.status = st;
     rs.argmax = C.RG;
     P.rowstat[pos] = rs;
-    if (stop) atomicOr(P.rej_mask + b, 1u << j);
+    unsigned long long bits = 1ull << j;
+    if (stop) bits |= 1ull << (32 + j);
+    state_or_release(P.state + b, bits);
 }
 
 // The last publisher of a row pair combines the row's G published partials (fp64) and takes the
@@ -393,13 +434,8 @@ __device__ __forceinline__ void row_decide(const Params& P, int b, int j, int x,
 }
 
 // Development timeline (debug builds, sd_debug_trace): slot i of the CTA's 8-word record gets
-// %globaltimer; word 7 = smid << 32 | flags (1 skipped, 2 last arriver, 4 stop).
+// %globaltimer; word 7 = smid << 32 | flags (1 skipped, 2 decider, 4 sampling task, 8 search).
 #if SD_STREAM_DEBUG
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 #define SD_TR(P, i)                                                                          \
     do {                                                                                     \
         if ((P).trace)                                                                       \
@@ -412,23 +448,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
             uint32_t smid;                                                                   \
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));                                \
             (P).trace[((static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + \
-                       blockIdx.x) * 8 + 7] = (static_cast<unsigned long long>(smid) << 32) | (f); \
-        }                                                                                    \
-    } while (0)
-// k_sample_req: records after k_row_stats' grid, one per request
-#define SD_TRS(P, i)                                                                         \
-    do {                                                                                     \
-        if ((P).trace) {                                                                     \
-            const size_t nbq = ((P).B + kGridY - 1) / kGridY;                                \
-            const size_t gA = static_cast<size_t>((P).nch) * ((P).B < kGridY ? (P).B : kGridY) * \
-                              ((P).k + 1) * nbq;                                             \
-            (P).trace[(gA + blockIdx.x) * 8 + (i)] = gtimer();                               \
+                       blockIdx.x) * 8 + 7] |= (static_cast<unsigned long long>(smid) << 32) | (f); \
         }                                                                                    \
     } while (0)
 #else
 #define SD_TR(P, i) do {} while (0)
 #define SD_TRF(P, f) do {} while (0)
-#define SD_TRS(P, i) do {} while (0)
 #endif
 
 // ---- tagged partials (k_row_stats with P.tagpub) --------------------------------------------
@@ -481,14 +506,14 @@ __device__ __forceinline__ void cluster_publish(const Params& P, const PartA& pa
             cl_send_part(cl_map(&s_parts[rank], 0), pa, cl_map(s_pbar, 0));
             SD_TR(P, 5);
             SD_TR(P, 6);
-            SD_TRF(P, 0);
         }
         return;
     }
     if (lane == 0) s_parts[0] = pa;
-    SD_SPIN(mbar_try_wait_cluster(s_pbar, 0), 1);
+    const bool ok = spin_until([&] { return mbar_try_wait_cluster(s_pbar, 0); }, 1);
     __syncwarp();
-    const Comb C = combine_parts<GREEDY, true>(s_parts, CL, lane);
+    Comb C = combine_parts<GREEDY, true>(s_parts, CL, lane);
+    if (!ok) C.flags |= kPartProtocol;
     if (C.flags & kPartSkipped) return;   // a peer saw a stop below j: the row is not needed
     if (P.G == 1) {                       // the cluster covers the row: decide at once
         if (lane == 0) {
@@ -509,7 +534,7 @@ __device__ __forceinline__ void cluster_publish(const Params& P, const PartA& pa
     }
     t = __shfl_sync(0xFFFFFFFFu, t, 0);
     if (t != static_cast<uint32_t>(P.G - 1)) {
-        if (lane == 0) { SD_TR(P, 6); SD_TRF(P, 0); }
+        if (lane == 0) SD_TR(P, 6);
         return;
     }
     row_decide<GREEDY>(P, b, j, x, lane);
@@ -517,305 +542,8 @@ __device__ __forceinline__ void cluster_publish(const Params& P, const PartA& pa
 }
 
 // ------------------------------------------------------------------------------------------
-// Kernel A: per-slice statistics + per-row acceptance decision
-//
-// CL > 1: the grid's x extent is G * CL (chunks padded with empty ones) in clusters of CL along
-// x.  A non-leader CTA sends its partial into the leader's (rank 0) shared memory with st.async
-// stores that complete bytes on the leader's mbarrier, then exits: no fence, no global atomic on
-// its path.  The leader
-// combines the CL partials; with G == 1 it decides at once, else it publishes the cluster partial
-// and takes the row ticket (the last of the G leaders decides).  Every CTA of a cluster arrives
-// exactly once, also when it skips, so the leader outlives every remote write into it.
-template <typename E, bool GREEDY, int CL, bool TAG>
-__global__ void __launch_bounds__(kThreads, GREEDY ? 8 : 6) k_row_stats(const Params P) {
-    using EL = Elt<E>;
-    constexpr int VEC = EL::VEC;
-    constexpr int NV = kMaxChunkBytes / kVecBytes / kThreads;   // 16-byte vectors per thread
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ __align__(8) uint64_t s_pbar;                    // CL > 1, leader: peer partials
-    __shared__ __align__(16) PartA s_parts[CL];
-    __shared__ __align__(16) PartA s_all[TAG ? kMaxTagNch : 1]; // TAG: the row's partials
-    __shared__ uint32_t s_tag;
-    __shared__ int s_flag;
-    __shared__ float s_d[2][kWarps];
-    __shared__ double s_s[2][kWarps];
-    __shared__ int s_gi[kWarps], s_f[kWarps];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nch = P.nch, kk = P.k;
-    // grid (chunk, request, position): blocks are scheduled x-fastest, so all requests'
-    // position 0 come first (position-major), without any integer division
-    // grid.y covers at most kGridY requests; grid.z = (k+1) * ceil(B / kGridY) (position-major)
-    const int c = blockIdx.x;
-    int b = blockIdx.y, j = blockIdx.z;
-    if (P.B > kGridY) {
-        const int nb = (P.B + kGridY - 1) / kGridY;
-        b += (j % nb) * kGridY;
-        j /= nb;
-        if (b >= P.B) return;
-    }
-    const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
-
-    const int rank = CL > 1 ? c % CL : 0;
-    // launched as a programmatic dependent of the previous kernel on the stream (P.chain): its
-    // results (the previous call's workspace reset, the caller's logits) are visible after this
-    if (P.chain) asm volatile("griddepcontrol.wait;" ::: "memory");
-    // (the earliest CTAs are the first row's: only they fold their start in)
-    if (P.prof_ts && tid == 0 && blockIdx.y == 0 && blockIdx.z == 0) prof_min(P.prof_ts);
-    if (tid == 0) {
-        SD_TR(P, 0);
-        const uint32_t m = j ? ld_relaxed_u32(P.rej_mask + b) : 0u;
-        if (TAG) s_tag = (ld_relaxed_u32(P.epoch) + 1u) | 0x80000000u;
-        s_flag = (m & ((1u << j) - 1u)) != 0u;
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        if (CL > 1 && rank == 0) mbar_init(&s_pbar, 1);
-        fence_mbar_init();
-        if (CL > 1 && rank == 0) mbar_arrive_expect_tx(&s_pbar, (CL - 1) * sizeof(PartA));
-    }
-    __syncthreads();
-    // the leader's barrier is initialised before any peer writes into it: every thread arrives on
-    // the cluster barrier now and waits on it before the first remote write (a skipping CTA at
-    // once, a working one after issuing its copies, so the wait overlaps the load).  Every thread
-    // takes part in both halves: a thread parked on a CTA barrier while its peers wait on the
-    // cluster barrier was measured to hang it.
-    if (CL > 1) cl_arrive_relaxed();
-    // The request already stopped before j: this row is never needed (laziness).  No ticket is
-    // taken: a needed row (j <= L) can never see a stop bit below j, so all its chunks arrive;
-    // the request's finalizer resets every ticket of the request for the next call.
-    if (s_flag) {
-        if (CL > 1) cl_wait_acquire();
-        if (tid == 0) {
-            SD_TR(P, 1);
-            SD_TRF(P, 1);
-            if (CL > 1) {
-                if (rank != 0) {
-                    PartA a{};
-                    a.flags = kPartSkipped;
-                    cl_send_part(cl_map(&s_parts[rank], 0), a, cl_map(&s_pbar, 0));
-                } else {
-                    SD_SPIN(mbar_try_wait_cluster(&s_pbar, 0), 2);
-                }
-            }
-            // tagged partials: the row's decider (last chunk) may be working -- say "skipped"
-            if (TAG && c != nch - 1) {
-                PartA a{};
-                a.flags = kPartSkipped;
-                write_tagged(P, pos, c, a, s_tag);
-            }
-        }
-        return;
-    }
-    if (tid == 0) SD_TR(P, 1);
-
-    const int c0 = c * P.CH;
-    const int len = max(0, min(P.CH, P.V - c0));   // CL > 1: empty padding chunks past V
-    const bool load_q = !GREEDY && j < kk;
-    const E* gp = static_cast<const E*>(P.p) + static_cast<int64_t>(pos) * P.ld_p + c0;
-    const E* gq = load_q ? static_cast<const E*>(P.q) +
-                               (static_cast<int64_t>(b) * kk + j) * P.ld_q + c0
-                         : nullptr;
-    E* sp = reinterpret_cast<E*>(smem);
-    E* sq = sp + P.CH;
-    const uint32_t bytes = static_cast<uint32_t>(len) * sizeof(E);
-    const uint32_t bulk = bytes & ~15u;
-    // p and q slices are copied by threads of different warps: bulk copies issued by one thread
-    // complete one after another (tools/tma_probe)
-    if (tid == 0) {
-        mbar_arrive_expect_tx(&bar[0], bulk);
-        if (bulk) bulk_g2s(sp, gp, bulk, &bar[0]);
-    } else if (tid == 32 && load_q) {
-        mbar_arrive_expect_tx(&bar[1], bulk);
-        if (bulk) bulk_g2s(sq, gq, bulk, &bar[1]);
-    }
-    for (int i = static_cast<int>(bulk / sizeof(E)) + tid; i < len; i += kThreads) {
-        sp[i] = gp[i];
-        if (load_q) sq[i] = gq[i];
-    }
-    const int x = (j < kk) ? P.ids[static_cast<size_t>(b) * kk + j] : -1;
-    if (CL > 1) cl_wait_acquire();   // (copies in flight) the leader's s_pbar is initialised
-    __syncthreads();
-
-    // ---- registers: NV vectors of p (and q) per thread; -inf past the slice end ------------
-    const int nfull = len / VEC;                 // complete vectors
-    const int nvv = (len + VEC - 1) / VEC;       // vectors incl. a ragged last one
-    float vp[NV][VEC];
-    SD_SPIN(mbar_try_wait(&bar[0], 0), 3);
-    if (tid == 0) SD_TR(P, 2);
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int g = tid + i * kThreads;
-        if (g < nfull) {
-            EL::unpack(*reinterpret_cast<const uint4*>(sp + g * VEC), vp[i]);
-        } else {
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) vp[i][e] = -INFINITY;
-            if (g < nvv) {   // ragged last vector (row end only)
-#pragma unroll
-                for (int e = 0; e < VEC; ++e)
-                    if (g * VEC + e < len) vp[i][e] = EL::one(sp, g * VEC + e);
-            }
-        }
-    }
-    int nf = 0;
-    float dP = -INFINITY, dQ = -INFINITY, sP = 0.0f, sQ = 0.0f;
-    float gbest = -INFINITY;
-    int gidx = INT_MAX;
-    if (GREEDY) {
-        float nanacc = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            float vm = -INFINITY;
-#pragma unroll
-            for (int e = 0; e < VEC; e += 2) {
-                nanacc = max3nan(nanacc, vp[i][e], vp[i][e + 1]);
-                vm = max3(vm, vp[i][e], vp[i][e + 1]);
-            }
-            if (vm > gbest) {   // ascending index within the thread: strict > keeps the first
-                int fe = 0;
-#pragma unroll
-                for (int e = VEC - 1; e >= 0; --e)
-                    if (vp[i][e] == vm) fe = e;
-                gbest = vm;
-                gidx = c0 + (tid + i * kThreads) * VEC + fe;
-            }
-        }
-        if (!(nanacc < INFINITY)) nf |= kPartNonfiniteP;
-    } else {
-        thread_stats<NV, VEC>(vp, P.c2, kPartNonfiniteP, dP, sP, nf);
-        if (load_q) {
-            float vq[NV][VEC];
-            SD_SPIN(mbar_try_wait(&bar[1], 0), 4);
-            if (tid == 0) SD_TR(P, 3);
-#pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                const int g = tid + i * kThreads;
-                if (g < nfull) {
-                    EL::unpack(*reinterpret_cast<const uint4*>(sq + g * VEC), vq[i]);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < VEC; ++e) vq[i][e] = -INFINITY;
-                    if (g < nvv) {
-#pragma unroll
-                        for (int e = 0; e < VEC; ++e)
-                            if (g * VEC + e < len) vq[i][e] = EL::one(sq, g * VEC + e);
-                    }
-                }
-            }
-            thread_stats<NV, VEC>(vq, P.c2, kPartNonfiniteQ, dQ, sQ, nf);
-        }
-    }
-
-    // ---- block reduction: warps, then warp 0 ---------------------------------------------
-    nf = __reduce_or_sync(0xFFFFFFFFu, nf);
-    if (GREEDY) {
-        float v = gbest;
-        int i = gidx;
-        warp_argmax(v, i);
-        if (lane == 0) {
-            s_d[0][warp] = v;
-            s_gi[warp] = i;
-            s_f[warp] = nf;
-        }
-    } else {
-        const float Dw = warp_max(dP), Ew = warp_max(dQ);
-        const double Sw = warp_sum(sP > 0.0f ? static_cast<double>(sP * ex2_approx(dP - Dw)) : 0.0);
-        const double Tw = warp_sum(sQ > 0.0f ? static_cast<double>(sQ * ex2_approx(dQ - Ew)) : 0.0);
-        if (lane == 0) {
-            s_d[0][warp] = Dw;
-            s_d[1][warp] = Ew;
-            s_s[0][warp] = Sw;
-            s_s[1][warp] = Tw;
-            s_f[warp] = nf;
-        }
-    }
-    __syncthreads();
-    if (tid == 0) SD_TR(P, 4);
-    if ((CL > 1 || TAG) && warp != 0) return;
-    if (warp == 0) {
-        const bool on = lane < kWarps;
-        const int f = __reduce_or_sync(0xFFFFFFFFu, on ? s_f[lane] : 0);
-        PartA pa;
-        if (GREEDY) {
-            float v = on ? s_d[0][lane] : -INFINITY;
-            int i = on ? s_gi[lane] : INT_MAX;
-            warp_argmax(v, i);
-            pa.M_p = v;
-            pa.M_q = -INFINITY;
-            pa.S_p = pa.S_q = 0.0;
-            pa.argmax = i;
-        } else {
-            const float wd = on ? s_d[0][lane] : -INFINITY, we = on ? s_d[1][lane] : -INFINITY;
-            const double ws = on ? s_s[0][lane] : 0.0, wt = on ? s_s[1][lane] : 0.0;
-            const float Dc = warp_max(wd), Ec = warp_max(we);
-            pa.S_p = warp_sum(ws > 0.0 ? ws * static_cast<double>(ex2_approx(wd - Dc)) : 0.0);
-            pa.S_q = warp_sum(wt > 0.0 ? wt * static_cast<double>(ex2_approx(we - Ec)) : 0.0);
-            pa.M_p = Dc;   // scaled maxima D (see prob_term)
-            pa.M_q = Ec;
-            pa.argmax = INT_MAX;
-        }
-        if (lane == 0) {
-            pa.zx_p = 0.0f;
-            pa.zx_q = 0.0f;
-            pa.flags = f;
-            if (x >= c0 && x < c0 + len) {
-                pa.zx_p = EL::one(sp, x - c0);
-                pa.zx_q = load_q ? EL::one(sq, x - c0) : 0.0f;
-                pa.flags |= kPartHasX;
-            }
-        }
-        if (CL > 1) {
-            cluster_publish<GREEDY, CL>(P, pa, s_parts, &s_pbar, rank, c / CL, b, j, x, lane);
-            return;
-        }
-        if (TAG) {
-            const uint32_t tag = s_tag;
-            if (c != nch - 1) {   // plain tagged stores, then exit: no fence, no ticket
-                if (lane == 0) {
-                    write_tagged(P, pos, c, pa, tag);
-                    SD_TR(P, 5);
-                    SD_TR(P, 6);
-                    SD_TRF(P, 0);
-                }
-                return;
-            }
-            // the row's last chunk decides: the other chunks of the row were dispatched before it
-            if (lane == 0) s_all[c] = pa;
-            for (int cc = lane; cc < nch - 1; cc += 32) {
-                PartA a;
-                SD_SPIN(read_tagged(P, pos, cc, tag, a), 9);
-                s_all[cc] = a;
-            }
-            __syncwarp();
-            const Comb C = combine_parts<GREEDY, true>(s_all, nch, lane);
-            if (lane == 0) SD_TR(P, 5);
-            if (!(C.flags & kPartSkipped) && lane == 0) decide<GREEDY>(P, b, j, x, C);
-            if (lane == 0) { SD_TR(P, 6); SD_TRF(P, 2); }
-            return;
-        }
-        if (lane == 0) {
-            P.partA[pos * nch + c] = pa;
-            uint32_t t;   // release: the partial is visible before the ticket
-            asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(P.ticketA + pos) : "memory");
-            s_flag = t == static_cast<uint32_t>(nch - 1);   // last arriver of the row
-            SD_TR(P, 5);
-        }
-    }
-    __syncthreads();
-    if (!s_flag || warp != 0) {
-        if (tid == 0) { SD_TR(P, 6); SD_TRF(P, 0); }
-        return;
-    }
-
-    row_decide<GREEDY>(P, b, j, x, lane);
-    if (tid == 0) { SD_TR(P, 6); SD_TRF(P, 2); }
-}
-
-// ------------------------------------------------------------------------------------------
-// Kernel B: residual (or bonus) inverse-CDF sample at the stop position L
-//
-// Residual terms of one 16-byte vector (raw bits of p and q), ascending token order:
+// Sampling (a6-a8): residual (or bonus) terms of one 16-byte vector (raw bits of p and q),
+// ascending token order:
 //   p(x) = 2^(z_p c2 - D_p) / S_p,  r(x) = max(0, p(x) - q(x)); r = p if !use_q.
 // Elements at or past `valid` are 0.  Returns the sequential fp32 sums of r and p (the order the
 // token search re-uses, so its partial sums are bit-identical).
@@ -919,16 +647,26 @@ __device__ __forceinline__ double2 warp_scan2(double2 v, int lane) {
     return v;
 }
 
-// One chunk of request b's sampling row pair (p_L, q_L) (whole CTA): stage chunk c (HBM; L2
-// when recent), compute r and p per 32-vector segment (warp scans, fp64 segment masses) and the
-// chunk's masses (a warp scan over segment pairs: the search's association), publish them and
-// take the request's ticket.  Returns (in every thread) whether this CTA is the request's last.
-// The mbarrier parities ph0 (p) / ph1 (q) advance with each use.
+__device__ __forceinline__ ResidParams resid_params(const RowStat& rs, bool use_q) {
+    ResidParams rp;
+    rp.nDp = -rs.M_p;
+    rp.nDq = use_q ? -rs.M_q : 0.0f;
+    rp.ip = static_cast<float>(1.0 / rs.S_p);
+    rp.iq = use_q ? static_cast<float>(1.0 / rs.S_q) : 0.0f;
+    rp.use_q = use_q ? 1 : 0;
+    return rp;
+}
+
+// Sampling chunk task c of request b at its stop position L (whole CTA): stage chunk c of
+// (p_L, q_L) (L2 when recent), compute r and p per 32-vector segment (warp scans, fp64 segment
+// masses) and the chunk's masses (a warp scan over segment pairs: the search's association),
+// publish them and take the request's sampling ticket.  Returns (in every thread) whether this
+// CTA finished the request's last chunk task.  The mbarrier parities ph0 (p) / ph1 (q) advance
+// with each use.
 template <typename E>
 __device__ __forceinline__ bool sample_chunk(const Params& P, unsigned char* smem, uint64_t* bar,
                                              uint32_t& ph0, uint32_t& ph1, double2* s_seg,
-                                             int* s_last, int b, int L, int c, const RowStat& rs,
-                                             bool hard) {
+                                             int* s_last, int b, int L, int c, const RowStat& rs) {
     using EL = Elt<E>;
     constexpr int VEC = EL::VEC;
     constexpr int SEGV = 32;
@@ -936,12 +674,7 @@ __device__ __forceinline__ bool sample_chunk(const Params& P, unsigned char* sme
     const int nch = P.nch, kk = P.k;
     const bool use_q = L < kk;
     const float c2 = P.c2;
-    ResidParams rp;
-    rp.nDp = -rs.M_p;
-    rp.nDq = use_q ? -rs.M_q : 0.0f;
-    rp.ip = static_cast<float>(1.0 / rs.S_p);
-    rp.iq = use_q ? static_cast<float>(1.0 / rs.S_q) : 0.0f;
-    rp.use_q = use_q ? 1 : 0;
+    const ResidParams rp = resid_params(rs, use_q);
     const E* gp = static_cast<const E*>(P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
     const E* gq = use_q ? static_cast<const E*>(P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q
                         : nullptr;
@@ -949,53 +682,51 @@ __device__ __forceinline__ bool sample_chunk(const Params& P, unsigned char* sme
     const int len = min(P.CH, P.V - c0);
     const int nvv = (len + VEC - 1) / VEC;            // vectors incl. a ragged last one
     const int nsg = (nvv + SEGV - 1) / SEGV;          // segments in this chunk
-    if (!hard) {
-        E* sp = reinterpret_cast<E*>(smem);
-        E* sq = sp + P.CH;
-        const uint32_t bytes = static_cast<uint32_t>(len) * sizeof(E);
-        const uint32_t bulk = bytes & ~15u;
-        if (tid == 0) {
-            mbar_arrive_expect_tx(&bar[0], bulk);
-            if (bulk) bulk_g2s(sp, gp + c0, bulk, &bar[0]);
-        } else if (tid == 32 && use_q) {
-            mbar_arrive_expect_tx(&bar[1], bulk);
-            if (bulk) bulk_g2s(sq, gq + c0, bulk, &bar[1]);
-        }
-        for (int i = static_cast<int>(bulk / sizeof(E)) + tid; i < len; i += kThreads) {
-            sp[i] = gp[c0 + i];
-            if (use_q) sq[i] = gq[c0 + i];
-        }
-        __syncthreads();
-        SD_SPIN(mbar_try_wait(&bar[0], ph0), 5);
-        ph0 ^= 1u;
-        if (use_q) {
-            SD_SPIN(mbar_try_wait(&bar[1], ph1), 6);
-            ph1 ^= 1u;
-        }
-        for (int sg = warp; sg < nsg; sg += kWarps) {
-            const int g = sg * SEGV + lane;
-            const int valid = min(VEC, max(0, len - g * VEC));
-            uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
-            if (g < nvv) {
-                up = *reinterpret_cast<const uint4*>(sp + g * VEC);
-                if (use_q) uq = *reinterpret_cast<const uint4*>(sq + g * VEC);
-            }
-            float r[VEC], pv[VEC], sr, spv;
-            resid_terms<E>(up, uq, valid, rp, c2, r, pv, sr, spv);
-            const double2 inc = warp_scan2(make_double2(sr, spv), lane);
-            if (lane == 31) s_seg[sg] = inc;
-        }
-        __syncthreads();
-        double2* gseg = P.segtab + (static_cast<size_t>(b) * nch + c) * P.nseg;
-        for (int sg = tid; sg < nsg; sg += kThreads) gseg[sg] = s_seg[sg];
-        if (warp == 0) {   // chunk masses: segment pairs, then a warp scan (the search's association)
-            const double2 a0 = 2 * lane < nsg ? s_seg[2 * lane] : make_double2(0.0, 0.0);
-            const double2 a1 = 2 * lane + 1 < nsg ? s_seg[2 * lane + 1] : make_double2(0.0, 0.0);
-            const double2 inc = warp_scan2(make_double2(__dadd_rn(a0.x, a1.x), __dadd_rn(a0.y, a1.y)), lane);
-            if (lane == 31) P.partB[static_cast<size_t>(b) * nch + c] = PartB{inc.x, inc.y};
-        }
-        __threadfence();
+    E* sp = reinterpret_cast<E*>(smem);
+    E* sq = sp + P.CH;
+    const uint32_t bytes = static_cast<uint32_t>(len) * sizeof(E);
+    const uint32_t bulk = bytes & ~15u;
+    if (tid == 0) {
+        mbar_arrive_expect_tx(&bar[0], bulk);
+        if (bulk) bulk_g2s(sp, gp + c0, bulk, &bar[0]);
+    } else if (tid == 32 && use_q) {
+        mbar_arrive_expect_tx(&bar[1], bulk);
+        if (bulk) bulk_g2s(sq, gq + c0, bulk, &bar[1]);
     }
+    for (int i = static_cast<int>(bulk / sizeof(E)) + tid; i < len; i += kThreads) {
+        sp[i] = gp[c0 + i];
+        if (use_q) sq[i] = gq[c0 + i];
+    }
+    __syncthreads();
+    mbar_wait(&bar[0], ph0);   // (the copies are in flight: they complete)
+    ph0 ^= 1u;
+    if (use_q) {
+        mbar_wait(&bar[1], ph1);
+        ph1 ^= 1u;
+    }
+    for (int sg = warp; sg < nsg; sg += kWarps) {
+        const int g = sg * SEGV + lane;
+        const int valid = min(VEC, max(0, len - g * VEC));
+        uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
+        if (g < nvv) {
+            up = *reinterpret_cast<const uint4*>(sp + g * VEC);
+            if (use_q) uq = *reinterpret_cast<const uint4*>(sq + g * VEC);
+        }
+        float r[VEC], pv[VEC], sr, spv;
+        resid_terms<E>(up, uq, valid, rp, c2, r, pv, sr, spv);
+        const double2 inc = warp_scan2(make_double2(sr, spv), lane);
+        if (lane == 31) s_seg[sg] = inc;
+    }
+    __syncthreads();
+    double2* gseg = P.segtab + (static_cast<size_t>(b) * nch + c) * P.nseg;
+    for (int sg = tid; sg < nsg; sg += kThreads) gseg[sg] = s_seg[sg];
+    if (warp == 0) {   // chunk masses: segment pairs, then a warp scan (the search's association)
+        const double2 a0 = 2 * lane < nsg ? s_seg[2 * lane] : make_double2(0.0, 0.0);
+        const double2 a1 = 2 * lane + 1 < nsg ? s_seg[2 * lane + 1] : make_double2(0.0, 0.0);
+        const double2 inc = warp_scan2(make_double2(__dadd_rn(a0.x, a1.x), __dadd_rn(a0.y, a1.y)), lane);
+        if (lane == 31) P.partB[static_cast<size_t>(b) * nch + c] = PartB{inc.x, inc.y};
+    }
+    __threadfence();
     __syncthreads();
     if (tid == 0) {
         const uint32_t t = atomicAdd(P.ticketB + b, 1u);
@@ -1006,24 +737,20 @@ __device__ __forceinline__ bool sample_chunk(const Params& P, unsigned char* sme
 }
 
 // The inverse CDF of request b over its published chunk and segment masses, chunk -> segment ->
-// token (warp 0 of the request's last chunk CTA; the result is valid in every lane).  The one
+// token (warp 0 of the request's last chunk task; the result is valid in every lane).  The one
 // found segment is recomputed with the identical routine, so the search sees exactly the masses
-// the main pass produced; clamps implement C-9, a zero residual falls back to p_L (C-6).
+// the chunk tasks produced; clamps implement C-9, a zero residual falls back to p_L (C-6).
+// *Rout = the mass of the distribution sampled (residual, or p at the bonus / C-6 fallback).
 template <typename E>
 __device__ __forceinline__ int32_t sample_search(const Params& P, int b, int L, const RowStat& rs,
-                                                 int32_t& status, int lane) {
+                                                 int32_t& status, int lane, double* Rout) {
     using EL = Elt<E>;
     constexpr int VEC = EL::VEC;
     constexpr int SEGV = 32;
     const int nch = P.nch, kk = P.k;
     const bool use_q = L < kk;
     const float c2 = P.c2;
-    ResidParams rp;
-    rp.nDp = -rs.M_p;
-    rp.nDq = use_q ? -rs.M_q : 0.0f;
-    rp.ip = static_cast<float>(1.0 / rs.S_p);
-    rp.iq = use_q ? static_cast<float>(1.0 / rs.S_q) : 0.0f;
-    rp.use_q = use_q ? 1 : 0;
+    const ResidParams rp = resid_params(rs, use_q);
     const E* gp = static_cast<const E*>(P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
     const E* gq = use_q ? static_cast<const E*>(P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q
                         : nullptr;
@@ -1042,6 +769,7 @@ __device__ __forceinline__ int32_t sample_search(const Params& P, int b, int L, 
     }
     const bool zero_res = use_q && !(carry.x > 0.0);        // C-6: fall back to p_L
     const double tot = zero_res ? carry.y : carry.x;
+    *Rout = tot;
     const uint4 w = verify_words(P.seed, static_cast<uint32_t>(L), P.round,
                                  P.rid_base + static_cast<uint64_t>(b));
     const double theta = unit24(w.y) * tot;                 // C-9: first x with C(x) > theta
@@ -1065,7 +793,7 @@ __device__ __forceinline__ int32_t sample_search(const Params& P, int b, int L, 
         run = __shfl_sync(0xFFFFFFFFu, icm, 31);
     }
     if (cstar < 0) cstar = clast;                           // rounding: last chunk with mass
-    // level 2: segments of chunk cstar (pairs per lane, warp scan: the main pass's association)
+    // level 2: segments of chunk cstar (pairs per lane, warp scan: the chunk task's association)
     const int cl = min(P.CH, P.V - cstar * P.CH);
     const int cnvv = (cl + VEC - 1) / VEC;
     const int cnsg = (cnvv + SEGV - 1) / SEGV;
@@ -1094,7 +822,7 @@ __device__ __forceinline__ int32_t sample_search(const Params& P, int b, int L, 
         sstar = 2 * lp + 1;
         th2 = th1 - __dadd_rn(exs, lm0);
     }
-    // recompute the segment exactly as the main pass did (r and p terms both; zero_res selects p)
+    // recompute the segment exactly as the chunk task did (r and p terms both; zero_res selects p)
     const int g = sstar * SEGV + lane;
     const int valid = min(VEC, max(0, cl - g * VEC));
     uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
@@ -1131,49 +859,330 @@ __device__ __forceinline__ int32_t sample_search(const Params& P, int b, int L, 
     return cstar * P.CH + (sstar * SEGV + ls) * VEC + fe;
 }
 
-// grid (chunk c, request b): the chunked sampler for rows longer than k_sample_req's on-chip
-// segment table (launched after k_row_stats with programmatic dependent launch).
+// One sampling chunk task (whole CTA); the CTA that completes the request's last task searches
+// and writes the request's outputs.  Hard-faulted requests have nothing to sample (the tail kernel
+// writes their outputs).
 template <typename E>
-__global__ void __launch_bounds__(kThreads) k_sample(const Params P) {
-    constexpr int MAXSEG = kMaxChunkBytes / 16 / 32;
+__device__ __forceinline__ void sample_task(const Params& P, unsigned char* smem, uint64_t* bar,
+                                            uint32_t& ph0, uint32_t& ph1, double2* s_seg,
+                                            int* s_last, int b, int L, int c) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const RowStat rs = load_cg(P.rowstat + static_cast<size_t>(b) * (P.k + 1) + L);
+    if (rs.status & kHard) return;
+    const bool last = sample_chunk<E>(P, smem, bar, ph0, ph1, s_seg, s_last, b, L, c, rs);
+    if (!last || warp != 0) return;
+    int32_t status = rs.status;
+    double R;
+    const int32_t tok = sample_search<E>(P, b, L, rs, status, lane, &R);
+    if (lane == 0) {
+        write_outputs(P, b, L, tok, status, false);
+        P.rres[b] = R;
+        SD_TRF(P, 8);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Kernel A: per-slice statistics + per-row acceptance decision (+ sampling chunk tasks)
+//
+// CL > 1: the grid's x extent is G * CL (chunks padded with empty ones) in clusters of CL along
+// x.  A non-leader CTA sends its partial into the leader's (rank 0) shared memory with st.async
+// stores that complete bytes on the leader's mbarrier, then exits: no fence, no global atomic on
+// its path.  The leader combines the CL partials; with G == 1 it decides at once, else it publishes
+// the cluster partial and takes the row ticket (the last of the G leaders decides).  Every CTA of
+// a cluster arrives exactly once, also when it skips, so the leader outlives every remote write
+// into it.
+// TAG (rows of 2..64 chunks, no cluster): every CTA that loads takes a start ticket on the row
+// right after issuing its copies; the one holding ticket nch-1 started last, so every other chunk
+// of the row has started (and never waits on anything): it polls their tagged partials and
+// decides.  Skipping CTAs take no ticket -- a needed row (j <= L) never sees a stop below j, so
+// all its chunks take tickets; an unneeded row may end without a decider.
+template <typename E, bool GREEDY, int CL, bool TAG>
+__global__ void __launch_bounds__(kThreads, GREEDY ? 8 : 6) k_row_stats(const Params P) {
+    using EL = Elt<E>;
+    constexpr int VEC = EL::VEC;
+    constexpr int NV = kMaxChunkBytes / kVecBytes / kThreads;   // 16-byte vectors per thread
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
-    __shared__ double2 s_seg[MAXSEG];
-    __shared__ int s_last;
+    __shared__ __align__(8) uint64_t s_pbar;                    // CL > 1, leader: peer partials
+    __shared__ __align__(16) PartA s_parts[CL];
+    __shared__ __align__(16) PartA s_all[TAG ? kMaxTagNch : 1]; // TAG: the row's partials
+    __shared__ uint32_t s_tag;
+    __shared__ int s_flag;
+    __shared__ float s_d[2][kWarps];
+    __shared__ double s_s[2][kWarps];
+    __shared__ int s_gi[kWarps], s_f[kWarps];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int kk = P.k;
-    const int c = blockIdx.x, b = blockIdx.y + blockIdx.z * kGridY;
-    if (b >= P.B) return;   // (whole CTA: the request's tickets count only real CTAs)
+    const int nch = P.nch, kk = P.k;
+    // grid (chunk, request, position): blocks are scheduled x-fastest, so all requests'
+    // position 0 come first (position-major), without any integer division
+    // grid.y covers at most kGridY requests; grid.z = (k+1) * ceil(B / kGridY) (position-major)
+    const int c = blockIdx.x;
+    int b = blockIdx.y, j = blockIdx.z;
+    if (P.B > kGridY) {
+        const int nb = (P.B + kGridY - 1) / kGridY;
+        b += (j % nb) * kGridY;
+        j /= nb;
+        if (b >= P.B) return;
+    }
+    const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
+
+    const int rank = CL > 1 ? c % CL : 0;
+    // launched as a programmatic dependent of the previous kernel on the stream (P.chain): its
+    // results (the previous call's workspace reset, the caller's logits) are visible after this
+    if (P.chain) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // (the earliest CTAs are the first row's: only they fold their start in)
+    if (P.prof_ts && tid == 0 && blockIdx.y == 0 && blockIdx.z == 0) prof_min(P.prof_ts);
     if (tid == 0) {
+        SD_TR(P, 0);
+        const unsigned long long s = j ? ld_relaxed_u64(P.state + b) : 0ull;
+        const uint32_t m = static_cast<uint32_t>(s >> 32);
+        const bool skip = (m & ((1u << j) - 1u)) != 0u;
+        if (TAG) s_tag = (ld_relaxed_u32(P.epoch) + 1u) | 0x80000000u;
+        s_flag = skip;
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
+        if (CL > 1 && rank == 0) mbar_init(&s_pbar, 1);
         fence_mbar_init();
+        if (CL > 1 && rank == 0) mbar_arrive_expect_tx(&s_pbar, (CL - 1) * sizeof(PartA));
     }
-    // programmatic dependent launch: this grid may start while k_row_stats drains; wait until
-    // every row decision of the primary grid is complete and visible
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (P.prof_ts && tid == 0 && blockIdx.x < 8) prof_min(P.prof_ts + 1);
-    if (P.tagpub && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
-        P.epoch[0] += 1u;   // k_row_stats is complete: the next call tags with a new value
-    // the next call's k_row_stats may be scheduled now (it waits for this grid to complete)
-    if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
-    const uint32_t mask = P.rej_mask[b];
-    const int L = mask ? __ffs(mask) - 1 : kk;
-    const RowStat rs = P.rowstat[static_cast<size_t>(b) * (kk + 1) + L];
-    const bool hard = (rs.status & kHard) != 0;
     __syncthreads();
-    uint32_t ph0 = 0, ph1 = 0;
-    if (!sample_chunk<E>(P, smem, bar, ph0, ph1, s_seg, &s_last, b, L, c, rs, hard) || warp != 0)
+    // the leader's barrier is initialised before any peer writes into it: every thread arrives on
+    // the cluster barrier now and waits on it before the first remote write (a skipping CTA at
+    // once, a working one after issuing its copies, so the wait overlaps the load).  Every thread
+    // takes part in both halves: a thread parked on a CTA barrier while its peers wait on the
+    // cluster barrier was measured to hang it.
+    if (CL > 1) cl_arrive_relaxed();
+    // The request already stopped before j: this row is never needed (laziness).
+    if (s_flag) {
+        if (CL > 1) cl_wait_acquire();
+        if (tid == 0) {
+            SD_TR(P, 1);
+            SD_TRF(P, 1);
+            if (CL > 1) {
+                if (rank != 0) {
+                    PartA a{};
+                    a.flags = kPartSkipped;
+                    cl_send_part(cl_map(&s_parts[rank], 0), a, cl_map(&s_pbar, 0));
+                } else {
+                    spin_until([&] { return mbar_try_wait_cluster(&s_pbar, 0); }, 2);
+                }
+            }
+        }
         return;
-    int32_t status = rs.status;
-    const int32_t tok = hard ? -1 : sample_search<E>(P, b, L, rs, status, lane);
-    if (lane == 0) {
-        write_outputs(P, b, L, tok, status, hard);
-        P.rej_mask[b] = 0u;      // leave the workspace zeroed for the next call
-        P.ticketB[b] = 0u;
-        for (int i = 0; i <= kk; ++i) P.ticketA[static_cast<size_t>(b) * (kk + 1) + i] = 0u;
     }
+    if (tid == 0) SD_TR(P, 1);
+
+    const int c0 = c * P.CH;
+    const int len = max(0, min(P.CH, P.V - c0));   // CL > 1: empty padding chunks past V
+    const bool load_q = !GREEDY && j < kk;
+    const E* gp = static_cast<const E*>(P.p) + static_cast<int64_t>(pos) * P.ld_p + c0;
+    const E* gq = load_q ? static_cast<const E*>(P.q) +
+                               (static_cast<int64_t>(b) * kk + j) * P.ld_q + c0
+                         : nullptr;
+    E* sp = reinterpret_cast<E*>(smem);
+    E* sq = sp + P.CH;
+    const uint32_t bytes = static_cast<uint32_t>(len) * sizeof(E);
+    const uint32_t bulk = bytes & ~15u;
+    // p and q slices are copied by threads of different warps: bulk copies issued by one thread
+    // complete one after another (tools/tma_probe)
+    uint32_t tk = 0;
+    if (tid == 0) {
+        mbar_arrive_expect_tx(&bar[0], bulk);
+        if (bulk) bulk_g2s(sp, gp, bulk, &bar[0]);
+        // start ticket (tagged rows): its result is consumed at publish time, so the round trip
+        // overlaps the load and the statistics
+        if (TAG) tk = ticket_relaxed(P.ticketA + pos);
+    } else if (tid == 32 && load_q) {
+        mbar_arrive_expect_tx(&bar[1], bulk);
+        if (bulk) bulk_g2s(sq, gq, bulk, &bar[1]);
+    }
+    for (int i = static_cast<int>(bulk / sizeof(E)) + tid; i < len; i += kThreads) {
+        sp[i] = gp[i];
+        if (load_q) sq[i] = gq[i];
+    }
+    const int x = (j < kk) ? P.ids[static_cast<size_t>(b) * kk + j] : -1;
+    if (CL > 1) cl_wait_acquire();   // (copies in flight) the leader's s_pbar is initialised
+    __syncthreads();
+
+    // ---- registers: NV vectors of p (and q) per thread; -inf past the slice end ------------
+    const int nfull = len / VEC;                 // complete vectors
+    const int nvv = (len + VEC - 1) / VEC;       // vectors incl. a ragged last one
+    float vp[NV][VEC];
+    mbar_wait(&bar[0], 0);   // (the copy is in flight: it completes)
+    if (tid == 0) SD_TR(P, 2);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int g = tid + i * kThreads;
+        if (g < nfull) {
+            EL::unpack(*reinterpret_cast<const uint4*>(sp + g * VEC), vp[i]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) vp[i][e] = -INFINITY;
+            if (g < nvv) {   // ragged last vector (row end only)
+#pragma unroll
+                for (int e = 0; e < VEC; ++e)
+                    if (g * VEC + e < len) vp[i][e] = EL::one(sp, g * VEC + e);
+            }
+        }
+    }
+    int nf = 0;
+    float dP = -INFINITY, dQ = -INFINITY, sP = 0.0f, sQ = 0.0f;
+    float gbest = -INFINITY;
+    int gidx = INT_MAX;
+    if (GREEDY) {
+        float nanacc = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            float vm = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < VEC; e += 2) {
+                nanacc = max3nan(nanacc, vp[i][e], vp[i][e + 1]);
+                vm = max3(vm, vp[i][e], vp[i][e + 1]);
+            }
+            if (vm > gbest) {   // ascending index within the thread: strict > keeps the first
+                int fe = 0;
+#pragma unroll
+                for (int e = VEC - 1; e >= 0; --e)
+                    if (vp[i][e] == vm) fe = e;
+                gbest = vm;
+                gidx = c0 + (tid + i * kThreads) * VEC + fe;
+            }
+        }
+        if (!(nanacc < INFINITY)) nf |= kPartNonfiniteP;
+    } else {
+        thread_stats<NV, VEC>(vp, P.c2, kPartNonfiniteP, dP, sP, nf);
+        if (load_q) {
+            float vq[NV][VEC];
+            mbar_wait(&bar[1], 0);
+            if (tid == 0) SD_TR(P, 3);
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int g = tid + i * kThreads;
+                if (g < nfull) {
+                    EL::unpack(*reinterpret_cast<const uint4*>(sq + g * VEC), vq[i]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) vq[i][e] = -INFINITY;
+                    if (g < nvv) {
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e)
+                            if (g * VEC + e < len) vq[i][e] = EL::one(sq, g * VEC + e);
+                    }
+                }
+            }
+            thread_stats<NV, VEC>(vq, P.c2, kPartNonfiniteQ, dQ, sQ, nf);
+        }
+    }
+
+    // ---- block reduction: warps, then warp 0 ---------------------------------------------
+    nf = __reduce_or_sync(0xFFFFFFFFu, nf);
+    if (GREEDY) {
+        float v = gbest;
+        int i = gidx;
+        warp_argmax(v, i);
+        if (lane == 0) {
+            s_d[0][warp] = v;
+            s_gi[warp] = i;
+            s_f[warp] = nf;
+        }
+    } else {
+        const float Dw = warp_max(dP), Ew = warp_max(dQ);
+        const double Sw = warp_sum(sP > 0.0f ? static_cast<double>(sP * ex2_approx(dP - Dw)) : 0.0);
+        const double Tw = warp_sum(sQ > 0.0f ? static_cast<double>(sQ * ex2_approx(dQ - Ew)) : 0.0);
+        if (lane == 0) {
+            s_d[0][warp] = Dw;
+            s_d[1][warp] = Ew;
+            s_s[0][warp] = Sw;
+            s_s[1][warp] = Tw;
+            s_f[warp] = nf;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) SD_TR(P, 4);
+    if ((CL > 1 || TAG) && warp != 0) return;
+    if (warp == 0) {
+        const bool on = lane < kWarps;
+        const int f = __reduce_or_sync(0xFFFFFFFFu, on ? s_f[lane] : 0);
+        PartA pa;
+        if (GREEDY) {
+            float v = on ? s_d[0][lane] : -INFINITY;
+            int i = on ? s_gi[lane] : INT_MAX;
+            warp_argmax(v, i);
+            pa.M_p = v;
+            pa.M_q = -INFINITY;
+            pa.S_p = pa.S_q = 0.0;
+            pa.argmax = i;
+        } else {
+            const float wd = on ? s_d[0][lane] : -INFINITY, we = on ? s_d[1][lane] : -INFINITY;
+            const double ws = on ? s_s[0][lane] : 0.0, wt = on ? s_s[1][lane] : 0.0;
+            const float Dc = warp_max(wd), Ec = warp_max(we);
+            pa.S_p = warp_sum(ws > 0.0 ? ws * static_cast<double>(ex2_approx(wd - Dc)) : 0.0);
+            pa.S_q = warp_sum(wt > 0.0 ? wt * static_cast<double>(ex2_approx(we - Ec)) : 0.0);
+            pa.M_p = Dc;   // scaled maxima D (see resid_terms)
+            pa.M_q = Ec;
+            pa.argmax = INT_MAX;
+        }
+        if (lane == 0) {
+            pa.zx_p = 0.0f;
+            pa.zx_q = 0.0f;
+            pa.flags = f;
+            if (x >= c0 && x < c0 + len) {
+                pa.zx_p = EL::one(sp, x - c0);
+                pa.zx_q = load_q ? EL::one(sq, x - c0) : 0.0f;
+                pa.flags |= kPartHasX;
+            }
+        }
+        if (CL > 1) {
+            cluster_publish<GREEDY, CL>(P, pa, s_parts, &s_pbar, rank, c / CL, b, j, x, lane);
+            return;
+        }
+        if (TAG) {
+            const uint32_t tag = s_tag;
+            tk = __shfl_sync(0xFFFFFFFFu, tk, 0);
+            if (tk != static_cast<uint32_t>(nch - 1)) {   // plain tagged stores, then exit
+                if (lane == 0) {
+                    write_tagged(P, pos, c, pa, tag);
+                    SD_TR(P, 5);
+                    SD_TR(P, 6);
+                }
+                return;
+            }
+            // the row's decider: every other chunk of the row took its ticket before this one,
+            // so it has started; its tagged partial arrives
+            if (lane == 0) s_all[c] = pa;
+            bool ok = true;
+            for (int cc = lane; cc < nch; cc += 32) {
+                if (cc == c) continue;
+                PartA a;
+                ok = spin_until([&] { return read_tagged(P, pos, cc, tag, a); }, 9) && ok;
+                s_all[cc] = a;
+            }
+            ok = __all_sync(0xFFFFFFFFu, ok);
+            __syncwarp();
+            Comb C = combine_parts<GREEDY, true>(s_all, nch, lane);
+            if (!ok) C.flags |= kPartProtocol;
+            if (lane == 0) SD_TR(P, 5);
+            if (!(C.flags & kPartSkipped) && lane == 0) decide<GREEDY>(P, b, j, x, C);
+            if (lane == 0) { SD_TR(P, 6); SD_TRF(P, 2); }
+            return;
+        }
+        if (lane == 0) {
+            P.partA[pos * nch + c] = pa;
+            uint32_t t;   // release: the partial is visible before the ticket
+            asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(P.ticketA + pos) : "memory");
+            s_flag = t == static_cast<uint32_t>(nch - 1);   // last arriver of the row
+            SD_TR(P, 5);
+        }
+    }
+    __syncthreads();
+    if (!s_flag || warp != 0) {
+        if (tid == 0) SD_TR(P, 6);
+        return;
+    }
+
+    row_decide<GREEDY>(P, b, j, x, lane);
+    if (tid == 0) { SD_TR(P, 6); SD_TRF(P, 2); }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1219,7 +1228,6 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
         }
         fence_mbar_init();
     }
-    if (tid == 0) SD_TRS(P, 0);
     // programmatic dependent launch: wait until every decision of k_row_stats is visible
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (P.prof_ts && tid == 0 && blockIdx.x < 8) prof_min(P.prof_ts + 1);
@@ -1227,8 +1235,7 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
         P.epoch[0] += 1u;   // k_row_stats is complete: the next call tags with a new value
     // the next call's k_row_stats may be scheduled now (it waits for this grid to complete)
     if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
-    if (tid == 0) SD_TRS(P, 1);
-    const uint32_t mask = P.rej_mask[b];
+    const uint32_t mask = static_cast<uint32_t>(__ldcg(P.state + b) >> 32);
     const int L = mask ? __ffs(mask) - 1 : kk;
     const RowStat rs = load_cg(P.rowstat + static_cast<size_t>(b) * (kk + 1) + L);
     const bool hard = (rs.status & kHard) != 0;
@@ -1285,7 +1292,6 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
                     const uint32_t ph = (n / kSRing) & 1;
                     mbar_wait(&full[sl][0], ph);
                     if (rp.use_q) mbar_wait(&full[sl][1], ph);
-                    if (tid == 0 && u == 0 && attempt == 0) SD_TRS(P, 3);
                     const uint4* sp4 = reinterpret_cast<const uint4*>(smem + static_cast<size_t>(sl) * 2 * kSUnitBytes);
                     const uint4* sq4 = sp4 + UV;
                     // warp w: segments SPW*w .. SPW*w+SPW-1 of the unit (one vector per lane
@@ -1332,7 +1338,6 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
                 }
             }
             __syncthreads();
-            if (tid == 0 && attempt == 0) SD_TRS(P, 4);
             // ---- block masses (32 segments each; warp tree sums) and the total --------------
             const int nblk = (nseg + 31) / 32;
             for (int bk = warp; bk < nblk; bk += NW) {
@@ -1356,7 +1361,10 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
                     carry = __dadd_rn(carry, __shfl_sync(0xFFFFFFFFu, v, 31));
                 }
                 const double tot = carry;
-                if (lane == 0) s_sel[1] = tot > 0.0;
+                if (lane == 0) {
+                    s_sel[1] = tot > 0.0;
+                    P.rres[b] = tot / rs.S_p;   // (trace) mass of the distribution sampled
+                }
                 if (tot > 0.0) {
                     const double theta = unit24(w.y) * tot;      // C-9: first x with C(x) > theta
                     int bsel = -1, blast = 0;
@@ -1415,7 +1423,6 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
             __syncthreads();
         }
         // ---- level 3: re-read the found segment, scan it, find the lane and the token -------
-        if (tid == 0) SD_TRS(P, 5);
         if (warp == 0) {
             const int sgsel = s_sel[0];
             const double th2 = s_th;
@@ -1469,9 +1476,70 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
             ot[i] = v;
         }
         if (P.out_status) P.out_status[b] = status;
-        P.rej_mask[b] = 0u;      // leave the workspace zeroed for the next call
+        P.state[b] = 0ull;       // leave the workspace zeroed for the next call
         for (int i = 0; i <= kk; ++i) P.ticketA[static_cast<size_t>(b) * (kk + 1) + i] = 0u;
-        SD_TRS(P, 2);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Kernel B, chunked form (rows longer than k_sample_req's on-chip segment table, V > 262144 fp32
+// / 524288 bf16): grid (chunk c, request b).  CTA (c, b) runs sampling chunk task c of request b
+// at its stop position L; the CTA completing the request's last task searches and writes the
+// outputs.  The request's last CTA to finish writes the outputs of a hard-faulted request and
+// resets the request's workspace words.
+template <typename E>
+__global__ void __launch_bounds__(kThreads) k_sample_chunked(const Params P) {
+    constexpr int MAXSEG = kMaxChunkBytes / 16 / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ __align__(16) double2 s_seg[MAXSEG];
+    __shared__ int s_last;
+
+    const int tid = threadIdx.x;
+    const int kk = P.k, nch = P.nch;
+    const int c = blockIdx.x, b = blockIdx.y + blockIdx.z * kGridY;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    // programmatic dependent launch: this grid may start while k_row_stats drains; wait until
+    // the primary grid is complete and its writes are visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (P.prof_ts && tid == 0 && blockIdx.x < 8 && blockIdx.y == 0 && blockIdx.z == 0)
+        prof_min(P.prof_ts + 1);
+    if (P.tagpub && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        P.epoch[0] += 1u;   // k_row_stats is complete: the next call tags with a new value
+    // the next call's k_row_stats may be scheduled now (it waits for this grid to complete)
+    if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
+    if (b >= P.B) return;
+    const unsigned long long s = __ldcg(P.state + b);
+    int L = settled_L(s, kk);
+    RowStat rs;
+    if (L >= 0) {
+        rs = load_cg(P.rowstat + static_cast<size_t>(b) * (kk + 1) + L);
+    } else {   // a broken protocol (never in a correct run): void the request
+        L = 0;
+        rs = RowStat{};
+        rs.status = kProtocol;
+    }
+    const bool hard = (rs.status & kHard) != 0;
+    __syncthreads();
+    if (!hard) {
+        uint32_t ph0 = 0, ph1 = 0;
+        sample_task<E>(P, smem, bar, ph0, ph1, s_seg, &s_last, b, L, c);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const uint32_t t = atomicAdd(P.tailT + b, 1u);
+        if (t == static_cast<uint32_t>(nch - 1)) {   // every sampling step of b is complete
+            if (hard) write_outputs(P, b, L, -1, rs.status, true);
+            P.state[b] = 0ull;   // leave the workspace zeroed for the next call
+            P.ticketB[b] = 0u;
+            P.tailT[b] = 0u;
+            for (int i = 0; i <= kk; ++i) P.ticketA[static_cast<size_t>(b) * (kk + 1) + i] = 0u;
+        }
     }
 }
 
@@ -1486,7 +1554,7 @@ __global__ void k_finalize_greedy(const Params P) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= P.B) return;
     const int kk = P.k;
-    const uint32_t mask = P.rej_mask[b];
+    const uint32_t mask = static_cast<uint32_t>(P.state[b] >> 32);
     const int L = mask ? __ffs(mask) - 1 : kk;
     const RowStat rs = P.rowstat[static_cast<size_t>(b) * (kk + 1) + L];
     const bool hard = (rs.status & kHard) != 0;
@@ -1498,8 +1566,31 @@ __global__ void k_finalize_greedy(const Params P) {
         ot[i] = v;
     }
     if (P.out_status) P.out_status[b] = rs.status;
-    P.rej_mask[b] = 0u;
+    P.state[b] = 0ull;
     for (int i = 0; i <= kk; ++i) P.ticketA[static_cast<size_t>(b) * (kk + 1) + i] = 0u;
+}
+
+// ------------------------------------------------------------------------------------------
+// sd_verify_trace: the statistics the last call on a workspace computed, per (b, j) thread.
+//   lam = ln 2 (D + log2 S)   (natural-log log-normaliser of softmax(z / T); D, S as in RowStat)
+__global__ void k_trace(const RowStat* rowstat, const double* rres, const int32_t* accept_len,
+                        int B, int k, double* lam_p, double* lam_q, double* a_out, double* R_out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * (k + 1)) return;
+    const int b = i / (k + 1), j = i % (k + 1);
+    const int L = accept_len[b];
+    const RowStat rs = rowstat[i];
+    const double ln2 = 0.69314718055994530942;
+    const bool reached = j <= L;
+    lam_p[i] = reached ? ln2 * (static_cast<double>(rs.M_p) + log2(rs.S_p)) : NAN;
+    if (j < k) {
+        lam_q[b * k + j] = reached ? ln2 * (static_cast<double>(rs.M_q) + log2(rs.S_q)) : NAN;
+        a_out[b * k + j] = reached ? rs.a : NAN;
+    }
+    if (j == 0) {
+        const RowStat rl = rowstat[static_cast<size_t>(b) * (k + 1) + L];
+        R_out[b] = (rl.status & kHard) ? NAN : rres[b];
+    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1543,6 +1634,7 @@ void record_event(cudaEvent_t ev, cudaStream_t st) {
     else
         cudaEventRecord(ev, st);
 }
+// (dynamic shared memory is at most 2 x 16 KB: below the 48 KB default, no opt-in attribute)
 template <typename E, bool G, int CL, bool TAG = false>
 static void launch_stats_cl(const Params& P, cudaStream_t st) {
     const int nb = (P.B + kGridY - 1) / kGridY;
@@ -1573,7 +1665,7 @@ static void launch_stats_cl(const Params& P, cudaStream_t st) {
 }
 template <typename E, bool G>
 static void launch_stats(const Params& P, cudaStream_t st) {
-    if (P.tagpub) {   // (tagged partials: rows of 9..64 chunks without clusters)
+    if (P.tagpub) {   // (tagged partials: rows of 2..64 chunks without clusters)
         launch_stats_cl<E, G, 1, true>(P, st);
         return;
     }
@@ -1585,48 +1677,46 @@ static void launch_stats(const Params& P, cudaStream_t st) {
     }
 }
 
+// k_sample_req's dynamic shared memory (ring + segment masses) needs the opt-in attribute, which
+// is per device: set it once per device (thread-safe).
+template <typename K>
+static cudaError_t ensure_smem_optin(K kernel, int bytes, std::atomic<uint64_t>& done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
+
 template <typename E>
 static cudaError_t launch_sampled(const Params& P, cudaStream_t st, cudaEvent_t ev0,
                                   cudaEvent_t ev1) {
     const size_t smem = 2 * static_cast<size_t>(P.CH) * sizeof(E);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_row_stats<E, false, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kMaxChunkBytes * 2);
-        cudaFuncSetAttribute(k_sample<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kMaxChunkBytes * 2);
-
-        attr = true;
-    }
     const int nb = (P.B + kGridY - 1) / kGridY;
+    const int nseg_row = (P.V + 32 * Elt<E>::VEC - 1) / (32 * Elt<E>::VEC);
+    static std::atomic<uint64_t> optin{0};
+    const size_t smB = static_cast<size_t>(kSRing) * 2 * kSUnitBytes + sizeof(double) * kSMaxSeg;
+    if (nseg_row <= kSMaxSeg) {
+        cudaError_t e = ensure_smem_optin(k_sample_req<E>, static_cast<int>(smB), optin);
+        if (e != cudaSuccess) return e;
+    }
     record_event(ev0, st);
     launch_stats<E, false>(P, st);
     record_event(ev1, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const int nseg_row = (P.V + 32 * (16 / static_cast<int>(sizeof(E))) - 1) / (32 * (16 / static_cast<int>(sizeof(E))));
-    if (nseg_row <= kSMaxSeg) {
-        static bool attr2 = false;
-        const size_t smB = static_cast<size_t>(kSRing) * 2 * kSUnitBytes + sizeof(double) * kSMaxSeg;
-        if (!attr2) {
-            cudaFuncSetAttribute(k_sample_req<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smB));
-            attr2 = true;
-        }
+    if (nseg_row <= kSMaxSeg)
         return launch_dependent(k_sample_req<E>, dim3(P.B), kSThreadsB + 32, smB, st, P);
-    }
-    return launch_dependent(k_sample<E>, dim3(P.nch, P.B < kGridY ? P.B : kGridY, nb), kThreads, smem,
-                            st, P);
+    return launch_dependent(k_sample_chunked<E>, dim3(P.nch, P.B < kGridY ? P.B : kGridY, nb),
+                            kThreads, smem, st, P);
 }
 
 template <typename E>
 static cudaError_t launch_greedy(const Params& P, cudaStream_t st, cudaEvent_t ev0,
                                  cudaEvent_t ev1) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_row_stats<E, true, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kMaxChunkBytes * 2);
-        attr = true;
-    }
     record_event(ev0, st);
     launch_stats<E, true>(P, st);
     record_event(ev1, st);
@@ -1644,14 +1734,23 @@ cudaError_t launch_verify(const Params& P, bool greedy, bool bf16, cudaStream_t 
                 : launch_sampled<float>(P, st, ev0, ev1);
 }
 
+cudaError_t launch_trace(const Params& P, const int32_t* accept_len, double* lam_p, double* lam_q,
+                         double* a, double* R, cudaStream_t st) {
+    const int n = P.B * (P.k + 1);
+    if (n > 0)
+        k_trace<<<(n + 255) / 256, 256, 0, st>>>(P.rowstat, P.rres, accept_len, P.B, P.k, lam_p,
+                                                 lam_q, a, R);
+    return cudaGetLastError();
+}
+
 // Device-side stand-in for a model forward of a given duration (star benchmarks): one thread
 // spins on %globaltimer.
 __global__ void k_spin_ns(uint64_t ns) {
-    uint64_t t0, t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    const uint64_t t0 = gtimer();
+    uint64_t t;
     do {
         __nanosleep(1000);
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        t = gtimer();
     } while (t - t0 < ns);
 }
 cudaError_t launch_spin_ns(uint64_t ns, cudaStream_t st) {

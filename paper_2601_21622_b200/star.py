@@ -27,6 +27,91 @@ def simulate(n_verifiers: int, n_slots: int, service_ms: float, return_ms: float
     return _stats_dict(st)
 
 
+def simulate_ex(service_ms, return_ms, n_slots: int, rounds: int) -> dict:
+    """sd_star_simulate_ex: heterogeneous star (per-verifier S_v, Z_v) under the fake transport;
+    adds the per-verifier services counted in the window."""
+    import numpy as np
+    S = np.ascontiguousarray(service_ms, np.float64)
+    Z = np.ascontiguousarray(return_ms, np.float64)
+    n = S.shape[0]
+    per = np.zeros(n, np.uint64)
+    st = _lib.StarStats()
+    check(_lib.load().sd_star_simulate_ex(n, n_slots, S.ctypes.data, Z.ctypes.data, rounds,
+                                          per.ctypes.data, ctypes.byref(st)), "sd_star_simulate_ex")
+    d = _stats_dict(st)
+    d["rounds_per_verifier"] = per.tolist()
+    return d
+
+
+def _pred_dict(p) -> dict:
+    return {f: getattr(p, f) for f, _ in _lib.Prediction._fields_}
+
+
+def analytics(beta, d: int, service_ms: float, return_ms: float, o_alone_per_ms: float) -> dict:
+    """sd_star_analytics: Sec. 4 closed forms (Eqs. 3-11), N_full and the admission bound N_max."""
+    import numpy as np
+    b = np.ascontiguousarray(beta, np.float64)
+    out = _lib.Prediction()
+    check(_lib.load().sd_star_analytics(b.shape[0], b.ctypes.data, d, float(service_ms),
+                                        float(return_ms), float(o_alone_per_ms),
+                                        ctypes.byref(out)), "sd_star_analytics")
+    return _pred_dict(out)
+
+
+class Scheduler:
+    """sd_sched_*: the star's host-side FIFO scheduler + online estimators, transport-free."""
+
+    def __init__(self, n_verifiers: int, k: int):
+        self._L = _lib.load()
+        self._h = ctypes.c_void_p()
+        check(self._L.sd_sched_create(ctypes.byref(self._h), n_verifiers, k), "sd_sched_create")
+
+    def push(self, verifier: int, slot: int, round: int, t_ms: float):
+        check(self._L.sd_sched_push(self._h, verifier, slot, round, float(t_ms)), "sd_sched_push")
+
+    def pop(self, now_ms: float):
+        v, s, r = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_uint64()
+        rc = self._L.sd_sched_pop(self._h, float(now_ms), ctypes.byref(v), ctypes.byref(s),
+                                  ctypes.byref(r))
+        if rc == _lib.SD_ERR_NOT_READY:
+            return None
+        check(rc, "sd_sched_pop")
+        return v.value, s.value, r.value
+
+    def service(self, verifier: int, t0_ms: float, t1_ms: float):
+        check(self._L.sd_sched_service(self._h, verifier, float(t0_ms), float(t1_ms)),
+              "sd_sched_service")
+
+    def observe(self, verifier: int, return_ms: float, accept_len=None):
+        import numpy as np
+        a = np.ascontiguousarray(accept_len if accept_len is not None else [], np.int32)
+        check(self._L.sd_sched_observe(self._h, verifier, float(return_ms),
+                                       a.ctypes.data if a.size else None, a.size),
+              "sd_sched_observe")
+
+    def stats(self) -> dict:
+        st = _lib.StarStats()
+        check(self._L.sd_sched_stats(self._h, ctypes.byref(st)), "sd_sched_stats")
+        return _stats_dict(st)
+
+    def predict(self, o_alone_per_ms: float) -> dict:
+        out = _lib.Prediction()
+        check(self._L.sd_sched_predict(self._h, float(o_alone_per_ms), ctypes.byref(out)),
+              "sd_sched_predict")
+        return _pred_dict(out)
+
+    def close(self):
+        if self._h:
+            self._L.sd_sched_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def _stats_dict(st) -> dict:
     return {"busy_fraction": st.busy_fraction, "mean_idle_ms": st.mean_idle_ms,
             "mean_wait_ms": st.mean_wait_ms, "window_ms": st.window_ms, "rounds": st.rounds}
@@ -44,7 +129,8 @@ def predicted(n_verifiers: int, service_ms: float, return_ms: float) -> dict:
 
 
 def unique_ids(world: int) -> bytes:
-    buf = ctypes.create_string_buffer(_lib.SD_STAR_ID_BYTES * (world - 1))
+    """Two communicator ids per (0, v) pair (draft -> verifier, verifier -> draft)."""
+    buf = ctypes.create_string_buffer(2 * _lib.SD_STAR_ID_BYTES * (world - 1))
     check(_lib.load().sd_star_unique_ids(world, buf), "sd_star_unique_ids")
     return buf.raw
 
@@ -56,7 +142,7 @@ def exchange_ids(rank: int, world: int, group=None) -> bytes:
     obj = [unique_ids(world) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     ids = obj[0]
-    if not isinstance(ids, bytes) or len(ids) != _lib.SD_STAR_ID_BYTES * (world - 1):
+    if not isinstance(ids, bytes) or len(ids) != 2 * _lib.SD_STAR_ID_BYTES * (world - 1):
         raise StarsdError("exchange_ids: malformed id blob")
     return ids
 
@@ -125,7 +211,8 @@ class Star:
               "sd_star_round")
 
     def poll(self, timeout_us: int = 0):
-        """Draft: next completed (verifier, slot, round) in FIFO order, or None."""
+        """Draft: next completed (verifier, slot, round) in FIFO order, or None.  Verifier: the
+        oldest round whose results have been sent, or None."""
         v, s, r = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_uint64()
         rc = self._L.sd_star_poll(self._h, ctypes.byref(v), ctypes.byref(s), ctypes.byref(r),
                                   timeout_us)
@@ -134,8 +221,9 @@ class Star:
         check(rc, "sd_star_poll")
         return v.value, s.value, r.value
 
-    def draft_begin(self, stream=None):
-        check(self._L.sd_star_draft_begin(self._h, self._stream(stream)), "sd_star_draft_begin")
+    def draft_begin(self, stream=None, verifier: int = 0):
+        check(self._L.sd_star_draft_begin_v(self._h, verifier, self._stream(stream)),
+              "sd_star_draft_begin")
 
     def draft_end(self, stream=None):
         check(self._L.sd_star_draft_end(self._h, self._stream(stream)), "sd_star_draft_end")
@@ -144,6 +232,19 @@ class Star:
         st = _lib.StarStats()
         check(self._L.sd_star_stats(self._h, ctypes.byref(st)), "sd_star_stats")
         return _stats_dict(st)
+
+    def observe(self, verifier: int, accept_len_host):
+        """Draft: feed a returned round's accept lengths (host) into the online beta estimate."""
+        import numpy as np
+        a = np.ascontiguousarray(accept_len_host, np.int32)
+        check(self._L.sd_star_observe(self._h, verifier, a.ctypes.data, a.size), "sd_star_observe")
+
+    def predict(self, o_alone_per_ms: float) -> dict:
+        """Draft: Sec. 4 closed forms on the online S(d), Z(d), beta; N_full and N_max."""
+        out = _lib.Prediction()
+        check(self._L.sd_star_predict(self._h, float(o_alone_per_ms), ctypes.byref(out)),
+              "sd_star_predict")
+        return _pred_dict(out)
 
     def close(self):
         if self._h:

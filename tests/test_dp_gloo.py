@@ -50,7 +50,7 @@ def test_gloo_world2_aggregation_and_handshake():
         assert mx == [11.0, 1.0]                 # MAX over ranks: the job's device time
         assert sm == [300.0]                     # SUM: units processed by all ranks
         assert rid == rank << 32
-        assert len(ids) == 128 * (world - 1)
+        assert len(ids) == 2 * 128 * (world - 1)   # one id per direction per (0, v) pair
     assert res[0][4] == res[1][4]                # every rank holds the draft's ids
     # disjoint 2^32-request Philox ranges
     assert res[1][3] - res[0][3] == 1 << 32

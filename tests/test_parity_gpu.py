@@ -229,17 +229,18 @@ def test_gpu_monte_carlo_matches_exact_outcome():
 
 
 @pytest.mark.parametrize("env,want", [
-    ({"STARSD_KERNEL": "stream"}, ("stream", None)),
+    ({"STARSD_FUSE": "0"}, ("two_launch", 0)),              # every sampling task in the tail
     ({"STARSD_ROWCLUSTER": "1"}, ("two_launch", 0)),        # cluster-free k_row_stats
     ({"STARSD_ROWCLUSTER": "-8"}, ("two_launch", 8)),       # clusters of 8 on every row (G > 1)
     ({"STARSD_ROWCLUSTER": "-2"}, ("two_launch", 2)),
-    ({"STARSD_PUBLISH": "ticket"}, ("two_launch", 0)),     # release-ordered partials + row ticket
+    ({"STARSD_PUBLISH_TICKET": "1"}, ("two_launch", 0)),   # release-ordered partials + row ticket
 ])
 def test_kernel_variants_match_the_oracle(env, want):
     """Kernel variants chosen by environment (once per process, so in a subprocess) against the
-    oracle on the default path's cases plus a Llama-3-vocabulary case: the opt-in persistent
-    stream kernel, the cluster-free k_row_stats (tagged partials), forced clusters whose row
-    partials meet through the global ticket (G = ceil(nch / CL) > 1), and the ticket publish."""
+    oracle on the default path's cases plus a Llama-3-vocabulary case: every sampling chunk task
+    in the tail kernel (no fused tasks), the cluster-free k_row_stats (tagged partials), forced
+    clusters whose row partials meet through the global ticket (G = ceil(nch / CL) > 1), and the
+    ticket publish."""
     import json
     import subprocess
     import sys
@@ -345,17 +346,15 @@ def test_profile_timestamps_bracket_the_stats_kernel():
 
 
 def test_one_workspace_serves_shapes_of_different_layout():
-    """A workspace sized for a large shape serves smaller shapes of a different layout (tagged
-    partials, clusters, tickets) once it is zero-filled again between shapes (include/starsd.h:
-    each call leaves only its own shape's zero region zeroed); calls of one shape reuse it as is."""
+    """A workspace sized for a large shape serves any sequence of smaller shapes of a different
+    layout (tagged partials, clusters, tickets) with no caller action: the library re-zeroes the
+    union of the two zero regions when the shape changes (include/starsd.h: the star's
+    per-slot workspaces see varying batch sizes)."""
     ws = sd.Workspace(16, 7, 128256, 1.0, device=DEV)
     cases = [(128256, 7, 16, 1.0), (128256, 7, 16, 1.0), (60000, 3, 8, 1.0), (32000, 5, 12, 1.0),
-             (128256, 7, 16, 0.0), (300000, 2, 2, 1.0), (128256, 7, 16, 1.0)]
-    prev = None
+             (128256, 7, 16, 0.0), (300000, 2, 2, 1.0), (128256, 7, 16, 1.0), (128256, 7, 4, 1.0),
+             (128256, 7, 16, 1.0), (32000, 5, 3, 0.0), (32000, 5, 12, 1.0)]
     for i, (V, k, B, T) in enumerate(cases):
-        if prev is not None and prev != (V, k, B, T == 0.0):
-            ws.buf.zero_()
-        prev = (V, k, B, T == 0.0)
         d = make_batch(V=V, k=k, B=B, T=max(T, 1e-3), kappa=30.0, seed=900 + i)
         p, q, ids = (torch.from_numpy(d[x]).to(DEV) for x in ("p", "q", "ids"))
         assert sd.workspace_size(B, k, V, T) <= ws.nbytes
