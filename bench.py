@@ -47,6 +47,16 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="auto", choices=["auto", "star", "dp"],
+                    help="N > 1: star (rank 0 drafts, ranks 1..N-1 verify; default) or dp "
+                         "(independent verifiers)")
+    ap.add_argument("--star-loopback", type=int, default=0,
+                    help="emulate a 1 -> N star in one process on one GPU (loopback transport)")
+    ap.add_argument("--payload", default="full", choices=["full", "qmeta"])
+    ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--draft-hidden", type=int, default=4096)
+    ap.add_argument("--o-alone", type=float, default=0.0,
+                    help="standalone target tokens/ms for the N_max admission bound")
     return ap.parse_args()
 
 
@@ -426,10 +436,197 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# --------------------------------------------------------------------------------- star ----
+def run_star(args):
+    """The 1 -> N-1 star (Alg. 1) on one node: rank 0 is the
+    draft, ranks 1..N-1 verify over per-pair NCCL communicators (or --star-loopback N: one process
+    plays the draft and N virtual verifiers on one GPU).  Draft service per verifier-round (SURVEY
+    8(d) B10): k LM-head-shaped bf16 GEMMs [B, H] x [H, V] (the draft model's cost, S(d) = d t_s,
+    Eq. 5) plus sd_draft_sample (NEXT-2) of the round's draft tokens from its q rows.  q rows come
+    from a seeded pool both sides regenerate identically (the verifier holds the matching target
+    rows), so acceptance follows the workload's kappa.  A step = one round for every (verifier,
+    slot) stream; W untimed steps, then K timed ones, each phase drained.  value = verified tokens
+    (L+1, all verifiers) / the max over ranks of each rank's CUDA-event window."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2601_21622_b200 as sd
+    from paper_2601_21622_b200 import star
+    from workload import make_batch_torch
+
+    rank, world, local = dist_env()
+    loop = args.star_loopback > 0
+    nver = args.star_loopback if loop else world - 1
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not loop:
+        dist.init_process_group("nccl", device_id=dev)
+    c = workload(args)
+    V, k, B, T = c["V"], c["k"], c["B"], c["T"]
+    tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
+    npool, slots = 2, args.slots
+    K, W = args.steps, max(3, args.warmup)
+
+    def pool_batch(v, i):
+        return make_batch_torch(V, k, B, T, c["kappa"] or 30.0, c["seed"] + 7919 * v + i, dev,
+                                dtype=args.dtype)
+
+    ids_x = star.exchange_ids(rank, world) if not loop else None
+    h = star.Star(0 if loop else rank, nver + 1, B, k, V, T, seed=21622, n_slots=slots, dtype=tdt,
+                  device=dev, ids=ids_x, transport="loopback" if loop else "nccl",
+                  timeout_ms=120000, payload=args.payload)
+    rid = lambda v, s: (v << 32) + s * B                                  # noqa: E731
+    pidx = lambda r, s: (r + s) % npool                                    # noqa: E731
+    total_rounds = W + K
+    s_main = torch.cuda.current_stream(dev)
+    if rank == 0:
+        qpool, ppool = {}, {}
+        for v in range(1, nver + 1):
+            for i in range(npool):
+                bt = pool_batch(v, i)
+                qpool[(v, i)] = bt["q"]
+                if loop:
+                    ppool[(v, i)] = bt["p"]
+                del bt
+        Wt = (torch.randn(args.draft_hidden, V, device=dev, dtype=torch.bfloat16) * 0.02)
+        hid = torch.randn(B, args.draft_hidden, device=dev, dtype=torch.bfloat16)
+        bufs = {(v, s): (torch.empty(B, dtype=torch.int32, device=dev),
+                         torch.empty(B, k + 1, dtype=torch.int32, device=dev))
+                for v in range(1, nver + 1) for s in range(slots)}
+        drafted = {}
+        tok_acc = torch.zeros((), dtype=torch.int64, device=dev)
+        per_v = torch.zeros(nver + 1, dtype=torch.int64, device=dev)
+        Lhost = {}
+
+        def draft_and_submit(v, s, r):
+            q = qpool[(v, pidx(r, s))]
+            h.draft_begin(verifier=v)
+            for _ in range(k):                                             # S(d) = d t_s
+                torch.matmul(hid, Wt)
+            ids, qm, _ = sd.draft_sample(q, T, seed=21622, round=r, request_id_base=rid(v, s),
+                                         want_qmeta=args.payload == "qmeta")
+            h.draft_end()
+            L, tok = bufs[(v, s)]
+            drafted[(v, s)] = (ids, qm, q)                                 # alive until the return
+            h.submit(v, s, r, ids, q, L, tok, request_id_base=rid(v, s),
+                     p=ppool[(v, pidx(r, s))] if loop else None, qmeta=qm)
+
+        def phase(r0, r1, count):
+            nonlocal tok_acc
+            for s in range(slots):
+                for v in range(1, nver + 1):
+                    draft_and_submit(v, s, r0)
+            left = nver * slots * (r1 - r0)
+            while left:
+                got = h.poll(timeout_us=120_000_000)
+                if got is None:
+                    raise RuntimeError("star: no return within 120 s")
+                v, s, r = got
+                left -= 1
+                L, _ = bufs[(v, s)]
+                if count:
+                    n = (L + 1).sum()
+                    tok_acc += n
+                    per_v[v] += n
+                    Lhost.setdefault(v, []).append(L.to("cpu", non_blocking=True))
+                if r + 1 < r1:
+                    draft_and_submit(v, s, r + 1)
+
+        phase(0, W, False)
+        torch.cuda.synchronize()
+        if not loop:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(s_main)
+            phase(W, total_rounds, True)
+            e1.record(s_main)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        tokens = float(tok_acc.item())
+        for v, Ls in Lhost.items():
+            for Lt in Ls:
+                h.observe(v, Lt.numpy())
+        st = h.stats()
+        try:
+            pred = h.predict(args.o_alone)
+        except sd.StarsdError:
+            pred = None
+        perv = (per_v.cpu().numpy()[1:] / (ms / 1000.0)).tolist()
+    else:
+        ppool = {i: pool_batch(rank, i)["p"] for i in range(npool)}
+        outs = {s: (torch.empty(B, dtype=torch.int32, device=dev),
+                    torch.empty(B, k + 1, dtype=torch.int32, device=dev)) for s in range(slots)}
+
+        def serve_phase(r0, r1):
+            for r in range(r0, r1):
+                for s in range(slots):
+                    # the slot's previous results must have left before its buffers are reused
+                    if r > r0:
+                        while h.poll(timeout_us=120_000_000) is None:
+                            raise RuntimeError("star verifier: send not done within 120 s")
+                    L, tok = outs[s]
+                    h.serve(s, r, B, ppool[pidx(r, s)], L, tok, request_id_base=rid(rank, s))
+            for _ in range(slots):
+                if h.poll(timeout_us=120_000_000) is None:
+                    raise RuntimeError("star verifier: send not done within 120 s")
+
+        serve_phase(0, W)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s_main)
+        serve_phase(W, total_rounds)
+        e1.record(s_main)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        tokens = 0.0
+    if not loop:
+        from paper_2601_21622_b200.dp import reduce_max_sum
+        (ms,), (tokens,) = reduce_max_sum([ms], [tokens], dev)
+    if rank == 0:
+        value = tokens / (ms / 1000.0)
+        S_ms = pred["service_ms"] if pred else None
+        Z_ms = pred["return_ms"] if pred else None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1 if loop else world,
+            "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": f"{args.config}: {c['name']}, star 1 -> {nver}"
+                                   + (" (loopback on one GPU)" if loop else ""),
+                       "vocab": V, "k": k, "batch_per_verifier": B, "temperature": T,
+                       "kappa": c["kappa"], "logits": args.dtype, "slots": slots,
+                       "payload": args.payload,
+                       "draft_standin": f"{k} x bf16 GEMM [{B},{args.draft_hidden}]x[{args.draft_hidden},{V}]"
+                                        " + sd_draft_sample per verifier-round",
+                       "parallelism": f"star: rank 0 draft, {nver} verifiers"},
+            "star": {"busy_fraction": st["busy_fraction"], "mean_idle_ms": st["mean_idle_ms"],
+                     "mean_wait_ms": st["mean_wait_ms"], "rounds": st["rounds"],
+                     "per_verifier_tokens_s": perv,
+                     "predicted": pred,
+                     "closed_form_busy": (min(1.0, nver * S_ms / (S_ms + Z_ms))
+                                          if S_ms and Z_ms is not None else None)},
+            "roofline": None,
+            "e2e": None,
+            "gpu_launches": None,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    h.close()
+    if not loop:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    world = dist_env()[1]
+    if args.star_loopback > 0 or (world > 1 and args.mode in ("auto", "star")):
+        run_star(args)
     else:
         run_ours(args)
 

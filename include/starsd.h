@@ -194,6 +194,66 @@ sd_status sd_verify_trace(const sd_shape* shape, float temperature, const void* 
                           const int32_t* accept_len, double* lam_p, double* lam_q, double* a,
                           double* R, cudaStream_t stream);
 
+/* ======================================================================================
+ * Draft side and exchange-minimal verify
+ *
+ * PAPER.md Alg. 2 ExpandLayer draws the draft tokens, and "the draft probabilities q_t(.)
+ * needed by the correction step are stored in the tree metadata".  The verify step needs
+ * of q_j only q_j(x_j) at every tested position, and the whole row only at the stop position L
+ * (the residual).  sd_qmeta carries the first part in the kernels' own arithmetic, so
+ * sd_verify_qmeta reads q rows only at L (a peer / remote pointer is fine) and takes decisions
+ * bit-identical to sd_verify on the same rows ("minimal-transfer design").
+ * log q_j(x_j) = ln 2 (zx c2 - D - log2 S), c2 = fl32(log2(e) / T).
+ * ====================================================================================== */
+typedef struct sd_qmeta_s {
+    double S;          /* sum_x 2^(z(x) c2 - D) over the q row (fp64 across threads)           */
+    float D;           /* the row's scaled maximum: max_x fl32(z(x) c2) (T = 0: the raw max)    */
+    float zx;          /* z(x_j): the draft token's logit (NaN if x_j is outside [0, V))        */
+    int32_t status;    /* SD_FAULT_NONFINITE / SD_FAULT_EMPTY_ROW of the q row, else 0         */
+    int32_t reserved;
+} sd_qmeta;            /* 24 bytes, 8-byte aligned */
+
+/* Bytes of workspace sd_draft_sample / sd_draft_qmeta need (host only). */
+sd_status sd_draft_workspace_size(const sd_shape* shape, float temperature, size_t* bytes);
+
+/*
+ * sd_draft_sample -- the draft-side sampler of the chain: x_j ~ softmax(q_logits[b][j] / T) for
+ * every (b, j), by inverse CDF in ascending token id (C-9) at theta = u * sum_y q_j(y),
+ * u = u24(w1) of Philox4x32-10 with key = seed and counter (0, round, rid_d lo, rid_d hi),
+ * rid_d = 2^63 + (request_id_base + b) k + j -- a counter domain disjoint from sd_verify's (whose
+ * request ids stay below 2^63), reading D-1 of DESIGN.md.  T = 0: argmax, lowest index.
+ *   q_logits  device [B][k][ld_q] (shape->ld_q; shape->ld_p is ignored), rows 16-byte aligned
+ *   out_ids   device [B][k] int32 (-1 for a row with NaN / +inf or no finite logit)
+ *   out_qmeta device [B][k] sd_qmeta of the sampled tokens, or NULL
+ *   out_status device [B][k] int32 fault bits of the q rows, or NULL
+ *   workspace >= sd_draft_workspace_size() bytes, zero-filled once (same contract as sd_verify's)
+ * Two passes over q (row statistics, then the sample) through the verify kernels themselves.
+ */
+sd_status sd_draft_sample(const void* q_logits, const sd_shape* shape, float temperature,
+                          uint64_t seed, uint64_t round, uint64_t request_id_base,
+                          int32_t* out_ids, sd_qmeta* out_qmeta, int32_t* out_status,
+                          void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* sd_draft_qmeta -- the metadata of GIVEN draft tokens draft_ids [B][k] (T > 0): one pass of row
+ * statistics over q_logits.  Same arguments as sd_draft_sample. */
+sd_status sd_draft_qmeta(const void* q_logits, const int32_t* draft_ids, const sd_shape* shape,
+                         float temperature, sd_qmeta* out_qmeta, void* workspace,
+                         size_t workspace_bytes, cudaStream_t stream);
+
+/*
+ * sd_verify_qmeta -- sd_verify with the draft rows given as metadata: q_meta [B][k] (device)
+ * replaces the statistics of q rows 0..k-1, and q_logits [B][k][ld_q] is read only at each
+ * request's stop position L < k (one row per rejecting request; it may point to a peer GPU's
+ * memory).  Same results as sd_verify on the same rows (bit-identical decisions and tokens when
+ * q_meta comes from sd_draft_sample / sd_draft_qmeta on those rows); same workspace (size and
+ * contract) as sd_verify.  T = 0 ignores q_meta and q_logits (greedy).
+ */
+sd_status sd_verify_qmeta(const void* p_logits, const void* q_logits, const sd_qmeta* q_meta,
+                          const int32_t* draft_ids, const sd_shape* shape, float temperature,
+                          uint64_t seed, uint64_t round, uint64_t request_id_base,
+                          int32_t* out_accept_len, int32_t* out_tokens, int32_t* out_status,
+                          void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
 /*
  * sd_debug_trace -- development instrumentation (library built with STARSD_BUILD_DEBUG=1;
  * otherwise ignored).  When device_buf != NULL, subsequent sd_verify calls on this thread write
@@ -236,7 +296,16 @@ typedef struct {
     float target_ms;     /* verifier-side stand-in for the target model's forward (t_v of Eq.
                             6): a device-side spin of this many ms on the verifier's
                             stream before each verify (0 = none); used by tools/star_bench.py  */
+    int32_t payload;     /* SD_STAR_PAYLOAD_FULL: ids + q rows [B_v][k][V] go out each round;
+                            SD_STAR_PAYLOAD_QMETA (NEXT-1, "minimal-transfer design"): ids +
+                            sd_qmeta [B_v][k] go out (24 bytes per draft token) and the verifier
+                            reads only its requests' stop rows q_L from the draft GPU's memory
+                            (NCCL transport: CUDA IPC peer mapping of per-(verifier, slot) staging
+                            buffers exchanged at create; loopback: the draft's q_logits directly),
+                            running sd_verify_qmeta                                            */
 } sd_star_config;
+
+enum { SD_STAR_PAYLOAD_FULL = 0, SD_STAR_PAYLOAD_QMETA = 1 };
 
 enum { SD_STAR_NCCL = 0, SD_STAR_LOOPBACK = 1 };
 
@@ -253,6 +322,9 @@ typedef struct {
     const void* q_logits;        /* draft: send source [B_v][k][V]; verifier: NULL -> receive    */
     int32_t* out_accept_len;     /* draft: receive dst [B_v]; verifier: local result [B_v]       */
     int32_t* out_tokens;         /* draft: receive dst [B_v][k+1]; verifier: local result        */
+    const struct sd_qmeta_s* q_meta; /* draft, QMETA payload: [B_v][k] metadata of draft_ids (from
+                                    sd_draft_sample / sd_draft_qmeta); q_logits must then stay
+                                    valid until the round returns (stop rows are read from it)  */
 } sd_round_desc;
 
 typedef struct {

@@ -74,6 +74,9 @@ def lib():
         L.sd_ref_accept_probs.restype = ctypes.c_int
         L.sd_ref_outcome_dist.argtypes = [vp, vp, vp, i32, i32, i32, i64, i64, i32, dbl, vp]
         L.sd_ref_outcome_dist.restype = ctypes.c_int
+        L.sd_ref_draft_sample.argtypes = [vp, i32, i32, i32, i64, i32, dbl, u64, u64, u64, vp, vp,
+                                          vp, vp]
+        L.sd_ref_draft_sample.restype = ctypes.c_int
         L.sd_ref_beta.argtypes = [vp, vp, i32, dbl]
         L.sd_ref_beta.restype = dbl
         L.sd_ref_softmax.argtypes = [vp, i32, dbl, vp]
@@ -177,6 +180,27 @@ def outcome_dist(p, q, ids, T, V=None):
     if rc != 0:
         raise ValueError("sd_ref_outcome_dist: invalid argument")
     return out
+
+
+def draft_sample(q, T, seed=0, round=0, rid_base=0, V=None):
+    """sd_ref_draft_sample on q [B, k, ld] (fp32, or uint16 raw bf16).  Returns (ids [B,k] int32,
+    log q(x) [B,k], CDF margin mu [B,k], status [B,k])."""
+    q = np.ascontiguousarray(q)
+    dtype = 1 if q.dtype == np.uint16 else 0
+    if dtype == 0:
+        q = np.ascontiguousarray(q, np.float32)
+    B, k, ld = q.shape
+    V = ld if V is None else V
+    ids = np.zeros((B, k), np.int32)
+    logq = np.zeros((B, k), np.float64)
+    mu = np.zeros((B, k), np.float64)
+    st = np.zeros((B, k), np.int32)
+    rc = lib().sd_ref_draft_sample(_ptr(q), B, k, V, ld, dtype, float(T), seed & (2**64 - 1),
+                                   round & (2**64 - 1), rid_base & (2**64 - 1), _ptr(ids),
+                                   _ptr(logq), _ptr(mu), _ptr(st))
+    if rc != 0:
+        raise ValueError("sd_ref_draft_sample: invalid argument")
+    return ids, logq, mu, st
 
 
 def beta(zp, zq, T=1.0):

@@ -495,3 +495,63 @@ void sd_ref_softmax(const float* z, int32_t V, double T, double* out) {
     double l = row_logsumexp(r, T);
     for (int32_t x = 0; x < V; ++x) out[x] = prob_of(r, x, T, l);
 }
+
+/* ------------------------------------------------------------------------------------------
+ * Draft-side sampler: the step before the verify path.  PAPER.md Alg. 2
+ * ExpandLayer draws the draft tokens from M_q, and "the draft probabilities q_t(.) needed
+ * by the correction step are stored in the tree metadata".  Chain form, per request b and
+ * position j (reading D-1 of DESIGN.md):
+ *   q_j = softmax(z_q,j / T);  x_j = the smallest token y (ascending id) with C(y) > theta,
+ *   C(y) = sum_{y' <= y} q_j(y'),  theta = u * sum_y q_j(y),  u = u24(w1) of Philox4x32-10 with
+ *   key = seed and counter (0, round, rid_d lo, rid_d hi), rid_d = 2^63 + (rid_base + b) k + j
+ *   (a counter domain disjoint from the verify step's, whose request ids stay below 2^63);
+ *   clamp to the last positive-mass token as in C-9.  T == 0: x_j = argmax (lowest index, C-5).
+ * out_logq[b][j] = log q_j(x_j) = z(x_j)/T - lambda_j (0 at T == 0); out_mu[b][j] (nullable) =
+ * min(theta - C(x-1), C(x) - theta) / sum q: the CDF-cell margin (tie rule).  Rows with NaN / +inf
+ * or no finite logit are faults (C-12): id -1, status bit set.
+ * ---------------------------------------------------------------------------------------- */
+int sd_ref_draft_sample(const void* q, int32_t B, int32_t k, int32_t V, int64_t ld_q,
+                        int32_t dtype, double T, uint64_t seed, uint64_t round, uint64_t rid_base,
+                        int32_t* out_ids, double* out_logq, double* out_mu, int32_t* out_status) {
+    if (!q || !out_ids || B < 0 || k < 1 || V < 2 || (dtype != 0 && dtype != 1) || !(T >= 0.0) ||
+        isinf(T))
+        return 1;
+    if (ld_q == 0) ld_q = V;
+    if (ld_q < V) return 1;
+    size_t esz = dtype == 0 ? 4 : 2;
+    double* buf = (double*)malloc(sizeof(double) * (size_t)V);
+    for (int32_t b = 0; b < B; ++b)
+        for (int32_t j = 0; j < k; ++j) {
+            size_t r = (size_t)b * k + j;
+            row_t qr = {(const char*)q + r * ld_q * esz, dtype, V};
+            int f = row_fault(qr);
+            if (out_status) out_status[r] = f;
+            if (out_mu) out_mu[r] = 1.0;
+            if (f) {
+                out_ids[r] = -1;
+                if (out_logq) out_logq[r] = 0.0;
+                continue;
+            }
+            if (T == 0.0) {
+                out_ids[r] = row_argmax(qr);
+                if (out_logq) out_logq[r] = 0.0;
+                continue;
+            }
+            double lam = row_logsumexp(qr, T);
+            int zr;
+            double S = sampling_dist(qr, lam, NULL, 0.0, T, buf, &zr);
+            uint64_t rid = ((uint64_t)1 << 63) + (rid_base + (uint64_t)b) * (uint64_t)k + (uint64_t)j;
+            double u;
+            sd_ref_uniforms(seed, 0u, round, rid, NULL, &u);
+            double theta = u * S, Cp, Ct;
+            int32_t x = inverse_cdf(buf, V, theta, &Cp, &Ct);
+            out_ids[r] = x;
+            if (out_logq) out_logq[r] = z_of(qr, x) / T - lam;
+            if (out_mu) {
+                double m1 = theta - Cp, m2 = Ct - theta;
+                out_mu[r] = (m1 < m2 ? m1 : m2) / S;
+            }
+        }
+    free(buf);
+    return 0;
+}

@@ -92,6 +92,13 @@ int sd_ref_outcome_dist(const void* p, const void* q, const int32_t* ids,
                         int32_t B, int32_t k, int32_t V, int64_t ld_p, int64_t ld_q, int32_t dtype,
                         double T, double* out);
 
+/* Draft-side sampler (NEXT-2): x_j ~ softmax(z_q,j / T) by inverse CDF on the
+ * Philox counter (0, round, 2^63 + (rid_base + b) k + j), word w1; T == 0 -> argmax.  See the .c
+ * file for the exact definition.  out_logq / out_mu / out_status are nullable. */
+int sd_ref_draft_sample(const void* q, int32_t B, int32_t k, int32_t V, int64_t ld_q,
+                        int32_t dtype, double T, uint64_t seed, uint64_t round, uint64_t rid_base,
+                        int32_t* out_ids, double* out_logq, double* out_mu, int32_t* out_status);
+
 /* Eq. (1): beta = sum_x min{p(x), q(x)} for p = softmax(zp/T), q = softmax(zq/T) (fp32 logits). */
 double sd_ref_beta(const float* zp, const float* zq, int32_t V, double T);
 /* softmax at temperature T of one fp32 logit row, fp64 out. */

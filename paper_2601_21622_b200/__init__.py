@@ -13,7 +13,8 @@ import torch
 from . import _lib
 from ._lib import StarsdError, check
 
-__all__ = ["verify", "verify_host", "verify_trace", "workspace_size", "plan", "philox_words",
+__all__ = ["verify", "verify_qmeta", "verify_host", "verify_trace", "draft_sample", "draft_qmeta",
+           "qmeta_fields", "workspace_size", "draft_workspace_size", "plan", "philox_words",
            "Workspace", "StarsdError", "version"]
 
 FAULT_BAD_DRAFT_ID, FAULT_NONFINITE, FAULT_EMPTY_ROW = 1, 2, 4
@@ -139,6 +140,131 @@ def verify(p: torch.Tensor, q: torch.Tensor | None, ids: torch.Tensor, temperatu
                                 request_id_base & (2**64 - 1), L.data_ptr(), tok.data_ptr(),
                                 st.data_ptr() if st is not None else None, ws.buf.data_ptr(),
                                 ws.nbytes, s.cuda_stream), "sd_verify")
+    return L, tok, st
+
+
+def _check_q(q: torch.Tensor):
+    if q.dim() != 3 or q.stride(-1) != 1 or q.stride(-2) != q.shape[-1] or \
+            q.stride(0) != q.shape[1] * q.shape[-1]:
+        raise StarsdError("q must be a contiguous [B, k, ld] tensor")
+    return _dtype_code(q)
+
+
+def draft_workspace_size(batch: int, k: int, vocab: int, temperature: float,
+                         dtype: torch.dtype = torch.float32) -> int:
+    code = _lib.SD_DTYPE_F32 if dtype == torch.float32 else _lib.SD_DTYPE_BF16
+    per16 = 4 if code == _lib.SD_DTYPE_F32 else 8
+    ld = (vocab + per16 - 1) // per16 * per16
+    n = ctypes.c_size_t()
+    check(_lib.load().sd_draft_workspace_size(ctypes.byref(_shape(batch, k, vocab, ld, ld, code)),
+                                              float(temperature), ctypes.byref(n)),
+          "sd_draft_workspace_size")
+    return n.value
+
+
+class DraftWorkspace(Workspace):
+    def __init__(self, batch, k, vocab, temperature, dtype=torch.float32, device=None, stream=None):
+        self.nbytes = draft_workspace_size(batch, k, vocab, temperature, dtype)
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            self.buf = torch.zeros(max(self.nbytes, 16), dtype=torch.uint8, device=device)
+
+
+_dws_cache: dict = {}
+
+
+def _draft_ws(q, stream, T):
+    B, k, V = q.shape
+    key = (str(q.device), stream.cuda_stream, B, k, V, T == 0.0, q.dtype)
+    ws = _dws_cache.get(key)
+    if ws is None:
+        ws = DraftWorkspace(B, k, V, T, q.dtype, q.device, stream)
+        _dws_cache[key] = ws
+    return ws
+
+
+def draft_sample(q: torch.Tensor, temperature: float, seed: int = 0, round: int = 0,
+                 request_id_base: int = 0, vocab: int | None = None, want_qmeta: bool = True,
+                 workspace=None, stream: torch.cuda.Stream | None = None):
+    """sd_draft_sample (NEXT-2): x_j ~ softmax(q[b, j] / T) for every (b, j).  q: [B, k, ld] CUDA
+    float32/bfloat16.  Returns (ids [B, k] int32, qmeta [B, k, 3] int64 holding sd_qmeta or None,
+    status [B, k] int32)."""
+    code = _check_q(q)
+    B, k, ld = q.shape
+    V = ld if vocab is None else vocab
+    ids = torch.empty(B, k, dtype=torch.int32, device=q.device)
+    qm = torch.empty(B, k, 3, dtype=torch.int64, device=q.device) if want_qmeta else None
+    st = torch.empty(B, k, dtype=torch.int32, device=q.device)
+    s = stream if stream is not None else torch.cuda.current_stream(q.device)
+    ws = workspace or _draft_ws(q, s, float(temperature))
+    sh = _shape(B, k, V, ld, ld, code)
+    check(_lib.load().sd_draft_sample(q.data_ptr(), ctypes.byref(sh), float(temperature),
+                                      seed & (2**64 - 1), round & (2**64 - 1),
+                                      request_id_base & (2**64 - 1), ids.data_ptr(),
+                                      qm.data_ptr() if qm is not None else None, st.data_ptr(),
+                                      ws.buf.data_ptr(), ws.nbytes, s.cuda_stream), "sd_draft_sample")
+    return ids, qm, st
+
+
+def draft_qmeta(q: torch.Tensor, ids: torch.Tensor, temperature: float, vocab: int | None = None,
+                workspace=None, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """sd_draft_qmeta: the sd_qmeta [B, k] (as int64 [B, k, 3]) of given draft tokens."""
+    code = _check_q(q)
+    B, k, ld = q.shape
+    V = ld if vocab is None else vocab
+    if ids.shape != (B, k) or ids.dtype != torch.int32 or not ids.is_contiguous():
+        raise StarsdError("ids must be a contiguous int32 [B, k] tensor")
+    qm = torch.empty(B, k, 3, dtype=torch.int64, device=q.device)
+    s = stream if stream is not None else torch.cuda.current_stream(q.device)
+    ws = workspace or _draft_ws(q, s, float(temperature))
+    sh = _shape(B, k, V, ld, ld, code)
+    check(_lib.load().sd_draft_qmeta(q.data_ptr(), ids.data_ptr(), ctypes.byref(sh),
+                                     float(temperature), qm.data_ptr(), ws.buf.data_ptr(),
+                                     ws.nbytes, s.cuda_stream), "sd_draft_qmeta")
+    return qm
+
+
+def qmeta_fields(qm: torch.Tensor) -> dict:
+    """Decode sd_qmeta records (int64 [..., 3]) into S (float64), D, zx (float32), status."""
+    flat = qm.reshape(-1, 3).contiguous()
+    S = flat[:, 0].view(torch.float64)
+    DZ = flat[:, 1].contiguous().view(torch.float32).reshape(-1, 2)
+    st = flat[:, 2].contiguous().view(torch.int32).reshape(-1, 2)[:, 0]
+    shp = qm.shape[:-1]
+    return {"S": S.reshape(shp), "D": DZ[:, 0].reshape(shp), "zx": DZ[:, 1].reshape(shp),
+            "status": st.reshape(shp)}
+
+
+def verify_qmeta(p: torch.Tensor, q: torch.Tensor, qmeta: torch.Tensor, ids: torch.Tensor,
+                 temperature: float, seed: int = 0, round: int = 0, request_id_base: int = 0,
+                 vocab: int | None = None, out: tuple | None = None,
+                 workspace: Workspace | None = None, stream: torch.cuda.Stream | None = None):
+    """sd_verify_qmeta (NEXT-1): verify with the draft rows as metadata; q [B, k, ld] is read only
+    at each request's stop position.  Same results as verify() on the same rows."""
+    B, k1, ld_p = p.shape
+    k = k1 - 1
+    if ids.shape != (B, k) or ids.dtype != torch.int32 or not ids.is_contiguous():
+        raise StarsdError("ids must be a contiguous int32 [B, k] tensor")
+    if p.stride(-1) != 1 or p.stride(-2) != ld_p or p.stride(0) != k1 * ld_p:
+        raise StarsdError("p must be contiguous [B, k+1, ld]")
+    code = _dtype_code(p)
+    _check_q(q)
+    if qmeta.shape != (B, k, 3) or qmeta.dtype != torch.int64 or not qmeta.is_contiguous():
+        raise StarsdError("qmeta must be int64 [B, k, 3] (sd_qmeta records)")
+    V = ld_p if vocab is None else vocab
+    if out is None:
+        out = (torch.empty(B, dtype=torch.int32, device=p.device),
+               torch.empty(B, k + 1, dtype=torch.int32, device=p.device),
+               torch.empty(B, dtype=torch.int32, device=p.device))
+    L, tok, st = out
+    s = stream if stream is not None else torch.cuda.current_stream(p.device)
+    ws = workspace or _workspace_for(p.device, s, B, k, V, float(temperature), p.dtype)
+    sh = _shape(B, k, V, ld_p, q.shape[-1], code)
+    check(_lib.load().sd_verify_qmeta(p.data_ptr(), q.data_ptr(), qmeta.data_ptr(), ids.data_ptr(),
+                                      ctypes.byref(sh), float(temperature), seed & (2**64 - 1),
+                                      round & (2**64 - 1), request_id_base & (2**64 - 1),
+                                      L.data_ptr(), tok.data_ptr(), st.data_ptr(),
+                                      ws.buf.data_ptr(), ws.nbytes, s.cuda_stream),
+          "sd_verify_qmeta")
     return L, tok, st
 
 

@@ -25,7 +25,8 @@ EXPORTS = ["sd_verify", "sd_verify_workspace_size", "sd_philox_uniforms", "sd_st
            "sd_star_simulate", "sd_verify_plan", "sd_verify_trace", "sd_star_simulate_ex",
            "sd_star_analytics", "sd_star_observe", "sd_star_predict", "sd_star_draft_begin_v",
            "sd_sched_create", "sd_sched_push", "sd_sched_pop", "sd_sched_service",
-           "sd_sched_observe", "sd_sched_stats", "sd_sched_predict", "sd_sched_destroy"]
+           "sd_sched_observe", "sd_sched_stats", "sd_sched_predict", "sd_sched_destroy",
+           "sd_draft_workspace_size", "sd_draft_sample", "sd_draft_qmeta", "sd_verify_qmeta"]
 
 
 class Shape(ctypes.Structure):
@@ -46,10 +47,12 @@ class StarConfig(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("n_slots", ctypes.c_int32),
                 ("max_shape", Shape), ("temperature", ctypes.c_float), ("seed", ctypes.c_uint64),
                 ("timeout_ms", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("transport", ctypes.c_int32), ("target_ms", ctypes.c_float)]
+                ("transport", ctypes.c_int32), ("target_ms", ctypes.c_float),
+                ("payload", ctypes.c_int32)]
 
 
 SD_STAR_NCCL, SD_STAR_LOOPBACK = 0, 1
+SD_STAR_PAYLOAD_FULL, SD_STAR_PAYLOAD_QMETA = 0, 1
 
 
 class RoundDesc(ctypes.Structure):
@@ -57,7 +60,7 @@ class RoundDesc(ctypes.Structure):
                 ("batch", ctypes.c_int32), ("request_id_base", ctypes.c_uint64),
                 ("p_logits", ctypes.c_void_p), ("draft_ids", ctypes.c_void_p),
                 ("q_logits", ctypes.c_void_p), ("out_accept_len", ctypes.c_void_p),
-                ("out_tokens", ctypes.c_void_p)]
+                ("out_tokens", ctypes.c_void_p), ("q_meta", ctypes.c_void_p)]
 
 
 class StarStats(ctypes.Structure):
@@ -101,6 +104,16 @@ def load():
     L.sd_verify_workspace_size.restype = st
     L.sd_verify_plan.argtypes = [ctypes.POINTER(Shape), ctypes.c_float, ctypes.POINTER(Plan)]
     L.sd_verify_plan.restype = st
+    L.sd_verify_qmeta.argtypes = [vp, vp, vp, vp, ctypes.POINTER(Shape), ctypes.c_float, u64, u64,
+                                  u64, vp, vp, vp, vp, sz, vp]
+    L.sd_verify_qmeta.restype = st
+    L.sd_draft_workspace_size.argtypes = [ctypes.POINTER(Shape), ctypes.c_float, ctypes.POINTER(sz)]
+    L.sd_draft_workspace_size.restype = st
+    L.sd_draft_sample.argtypes = [vp, ctypes.POINTER(Shape), ctypes.c_float, u64, u64, u64, vp, vp,
+                                  vp, vp, sz, vp]
+    L.sd_draft_sample.restype = st
+    L.sd_draft_qmeta.argtypes = [vp, vp, ctypes.POINTER(Shape), ctypes.c_float, vp, vp, sz, vp]
+    L.sd_draft_qmeta.restype = st
     L.sd_verify_trace.argtypes = [ctypes.POINTER(Shape), ctypes.c_float, vp, vp, vp, vp, vp, vp, vp]
     L.sd_verify_trace.restype = st
     L.sd_philox_uniforms.argtypes = [u64, u64, vp, vp, i32, vp, vp]

@@ -22,6 +22,10 @@ cudaError_t launch_philox(uint64_t seed, uint64_t round, const uint32_t* pos, co
                           int n, uint32_t* out, cudaStream_t st);
 cudaError_t launch_trace(const Params& P, const int32_t* accept_len, double* lam_p, double* lam_q,
                          double* a, double* R, cudaStream_t st);
+cudaError_t launch_qmeta(const Params& P, bool bf16, const int32_t* ids, QMeta* out,
+                         cudaStream_t st);
+cudaError_t qmeta_gather(const Params& P, bool bf16, const int32_t* ids, QMeta* out,
+                         cudaStream_t st);
 
 static thread_local char g_err[512] = "";
 static thread_local cudaEvent_t* g_prof_ev = nullptr;
@@ -167,11 +171,11 @@ sd_status sd_verify_workspace_size(const sd_shape* shape, float temperature, siz
     return SD_OK;
 }
 
-sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* draft_ids,
-                    const sd_shape* shape, float temperature, uint64_t seed, uint64_t round,
-                    uint64_t request_id_base, int32_t* out_accept_len, int32_t* out_tokens,
-                    int32_t* out_status, void* workspace, size_t workspace_bytes,
-                    cudaStream_t stream) {
+static sd_status verify_impl(const void* p_logits, const void* q_logits, const QMeta* qmeta,
+                             const int32_t* draft_ids, const sd_shape* shape, float temperature,
+                             uint64_t seed, uint64_t round, uint64_t request_id_base,
+                             int32_t* out_accept_len, int32_t* out_tokens, int32_t* out_status,
+                             void* workspace, size_t workspace_bytes, cudaStream_t stream) {
     clear_error();
     int esz;
     sd_status s = check_shape(shape, temperature, &esz);
@@ -180,6 +184,8 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     const bool greedy = temperature == 0.0f;
     if (!p_logits) return fail(SD_ERR_INVALID_ARGUMENT, "p_logits is NULL");
     if (!greedy && !q_logits) return fail(SD_ERR_INVALID_ARGUMENT, "q_logits is NULL (T > 0)");
+    if (!greedy && qmeta && (reinterpret_cast<uintptr_t>(qmeta) & 7u))
+        return fail(SD_ERR_INVALID_ARGUMENT, "q_meta not 8-byte aligned");
     if (!draft_ids) return fail(SD_ERR_INVALID_ARGUMENT, "draft_ids is NULL");
     if (!out_accept_len || !out_tokens)
         return fail(SD_ERR_INVALID_ARGUMENT, "out_accept_len / out_tokens is NULL");
@@ -203,6 +209,7 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     fill_params(P, shape, esz, temperature, workspace);
     P.p = p_logits;
     P.q = greedy ? nullptr : q_logits;
+    P.qmeta = greedy ? nullptr : qmeta;
     P.ids = draft_ids;
     P.seed = seed;
     P.round = round;
@@ -216,6 +223,124 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     cudaError_t e = launch_verify(P, greedy, shape->dtype == SD_DTYPE_BF16, stream, ev0, ev1);
     if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
     return SD_OK;
+}
+
+sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* draft_ids,
+                    const sd_shape* shape, float temperature, uint64_t seed, uint64_t round,
+                    uint64_t request_id_base, int32_t* out_accept_len, int32_t* out_tokens,
+                    int32_t* out_status, void* workspace, size_t workspace_bytes,
+                    cudaStream_t stream) {
+    return verify_impl(p_logits, q_logits, nullptr, draft_ids, shape, temperature, seed, round,
+                       request_id_base, out_accept_len, out_tokens, out_status, workspace,
+                       workspace_bytes, stream);
+}
+
+sd_status sd_verify_qmeta(const void* p_logits, const void* q_logits, const sd_qmeta* q_meta,
+                          const int32_t* draft_ids, const sd_shape* shape, float temperature,
+                          uint64_t seed, uint64_t round, uint64_t request_id_base,
+                          int32_t* out_accept_len, int32_t* out_tokens, int32_t* out_status,
+                          void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+    static_assert(sizeof(sd_qmeta) == sizeof(QMeta), "sd_qmeta layout");
+    if (temperature != 0.0f && !q_meta) {
+        clear_error();
+        return fail(SD_ERR_INVALID_ARGUMENT, "q_meta is NULL (T > 0)");
+    }
+    return verify_impl(p_logits, q_logits, reinterpret_cast<const QMeta*>(q_meta), draft_ids,
+                       shape, temperature, seed, round, request_id_base, out_accept_len,
+                       out_tokens, out_status, workspace, workspace_bytes, stream);
+}
+
+// ---- draft side (NEXT-2): the q rows as k = 0 "requests" of the verify kernels ----------------
+// Row r = b k + j of q_logits is request r of an internal call with k = 0: k_row_stats computes its
+// statistics exactly as it does for a verify's q rows (so the metadata is bit-identical to what a
+// full verify computes), and k_sample_req's bonus path samples it by inverse CDF with the counter
+// (0, round, 2^63 + request_id_base k + r) (reading D-1) -- or k_finalize_greedy takes its argmax.
+static WsLayout draft_layout(const sd_shape* shape, int esz, size_t* total) {
+    const int32_t R = shape->batch * shape->k;
+    const WsLayout w = ws_layout(R, 0, shape->vocab, esz);
+    *total = w.total + align16(sizeof(int32_t) * (size_t)R);
+    return w;
+}
+
+sd_status sd_draft_workspace_size(const sd_shape* shape, float temperature, size_t* bytes) {
+    clear_error();
+    int esz;
+    sd_status s = check_shape(shape, temperature, &esz);
+    if (s != SD_OK) return s;
+    if (!bytes) return fail(SD_ERR_INVALID_ARGUMENT, "bytes is NULL");
+    if ((int64_t)shape->batch * shape->k >= (1LL << 31))
+        return fail(SD_ERR_UNSUPPORTED, "batch * k too large");
+    draft_layout(shape, esz, bytes);
+    return SD_OK;
+}
+
+static sd_status draft_call(const void* q_logits, const int32_t* ids_in, const sd_shape* shape,
+                            float temperature, uint64_t seed, uint64_t round,
+                            uint64_t request_id_base, int32_t* out_ids, sd_qmeta* out_qmeta,
+                            int32_t* out_status, void* workspace, size_t workspace_bytes,
+                            cudaStream_t stream) {
+    int esz;
+    sd_status s = check_shape(shape, temperature, &esz);
+    if (s != SD_OK) return s;
+    if (shape->batch == 0) return SD_OK;
+    if (!q_logits || !workspace) return fail(SD_ERR_INVALID_ARGUMENT, "q_logits / workspace NULL");
+    if (!aligned16(q_logits) || !aligned16(workspace) ||
+        (out_qmeta && (reinterpret_cast<uintptr_t>(out_qmeta) & 7u)))
+        return fail(SD_ERR_INVALID_ARGUMENT, "q_logits / workspace / out_qmeta misaligned");
+    size_t need;
+    const WsLayout w = draft_layout(shape, esz, &need);
+    if (workspace_bytes < need)
+        return fail(SD_ERR_INVALID_ARGUMENT, "workspace_bytes=%zu < required %zu", workspace_bytes, need);
+    const bool greedy = temperature == 0.0f;
+    sd_shape in = *shape;                     // internal: R rows, k = 0, the q stride as p stride
+    in.batch = shape->batch * shape->k;
+    in.k = 0;
+    in.ld_p = shape->ld_q ? shape->ld_q : shape->vocab;
+    in.ld_q = in.ld_p;
+    s = ws_prepare(workspace, WsSig{in.batch, 0, in.vocab, esz, greedy, w.zero_bytes}, stream);
+    if (s != SD_OK) return s;
+    Params P{};
+    fill_params(P, &in, esz, temperature, workspace);
+    P.p = q_logits;
+    P.q = nullptr;
+    P.ids = nullptr;
+    P.seed = seed;
+    P.round = round;
+    P.rid_base = (1ull << 63) + request_id_base * static_cast<uint64_t>(shape->k);
+    P.out_L = reinterpret_cast<int32_t*>(static_cast<char*>(workspace) + w.total);
+    P.out_status = out_status;
+    const bool bf16 = shape->dtype == SD_DTYPE_BF16;
+    cudaError_t e;
+    if (ids_in) {                              // metadata of given tokens (no sampling)
+        e = launch_qmeta(P, bf16, ids_in, reinterpret_cast<QMeta*>(out_qmeta), stream);
+    } else {
+        P.out_tok = out_ids;
+        e = launch_verify(P, greedy, bf16, stream, nullptr, nullptr);
+        if (e == cudaSuccess && out_qmeta)
+            e = qmeta_gather(P, bf16, out_ids, reinterpret_cast<QMeta*>(out_qmeta), stream);
+    }
+    if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return SD_OK;
+}
+
+sd_status sd_draft_sample(const void* q_logits, const sd_shape* shape, float temperature,
+                          uint64_t seed, uint64_t round, uint64_t request_id_base,
+                          int32_t* out_ids, sd_qmeta* out_qmeta, int32_t* out_status,
+                          void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+    clear_error();
+    if (!out_ids) return fail(SD_ERR_INVALID_ARGUMENT, "out_ids is NULL");
+    return draft_call(q_logits, nullptr, shape, temperature, seed, round, request_id_base, out_ids,
+                      out_qmeta, out_status, workspace, workspace_bytes, stream);
+}
+
+sd_status sd_draft_qmeta(const void* q_logits, const int32_t* draft_ids, const sd_shape* shape,
+                         float temperature, sd_qmeta* out_qmeta, void* workspace,
+                         size_t workspace_bytes, cudaStream_t stream) {
+    clear_error();
+    if (!draft_ids || !out_qmeta) return fail(SD_ERR_INVALID_ARGUMENT, "draft_ids / out_qmeta NULL");
+    if (temperature == 0.0f) return fail(SD_ERR_INVALID_ARGUMENT, "sd_draft_qmeta: T > 0 only");
+    return draft_call(q_logits, draft_ids, shape, temperature, 0, 0, 0, nullptr, out_qmeta,
+                      nullptr, workspace, workspace_bytes, stream);
 }
 
 sd_status sd_verify_trace(const sd_shape* shape, float temperature, const void* workspace,

@@ -343,6 +343,10 @@ struct sd_star {
     int esz = 4;
     bool loop = false;                       // SD_STAR_LOOPBACK
     bool dead = false;                       // communicators aborted (timeout / NCCL error)
+    bool qm = false;                         // SD_STAR_PAYLOAD_QMETA
+    std::vector<void*> qstage;               // draft, NCCL + QMETA: per (v, slot) q rows, IPC-exported
+    std::vector<void*> qpeer;                // verifier, QMETA: the draft's staging, IPC-mapped
+    std::vector<void*> qmeta_buf;            // verifier, QMETA: received sd_qmeta [B][k] per slot
     // draft: index v (1..world-1); verifier: index 0.  down = draft -> verifier, up = back.
     std::vector<ncclComm_t> down, up;
     std::vector<cudaStream_t> sdown, sup;
@@ -436,12 +440,17 @@ static sd_status alloc_staging(sd_star* h, int n) {
         void *q = nullptr, *w = nullptr;
         int32_t *idb = nullptr, *lb = nullptr, *tb = nullptr;
         cudaEvent_t e0, e1, e2;
-        SD_CUDA(cudaMalloc(&q, B * k * V * h->esz));
+        if (!h->qm) SD_CUDA(cudaMalloc(&q, B * k * V * h->esz));   // (QMETA: no q rows arrive)
         SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&idb), B * k * sizeof(int32_t)));
         SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&lb), B * sizeof(int32_t)));
         SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&tb), B * (k + 1) * sizeof(int32_t)));
         SD_CUDA(cudaMalloc(&w, h->ws_bytes));
         SD_CUDA(cudaMemset(w, 0, h->ws_bytes));
+        if (h->qm) {
+            void* m = nullptr;
+            SD_CUDA(cudaMalloc(&m, B * k * sizeof(sd_qmeta)));
+            h->qmeta_buf.push_back(m);
+        }
         SD_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
         SD_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
         SD_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
@@ -458,6 +467,7 @@ static sd_status alloc_staging(sd_star* h, int n) {
 }
 
 static sd_status star_init(sd_star* h, const void* ids);
+static sd_status exchange_qstage(sd_star* h);
 
 static ncclDataType_t nccl_dtype(sd_dtype d) { return d == SD_DTYPE_F32 ? ncclFloat32 : ncclBfloat16; }
 
@@ -496,6 +506,11 @@ sd_status sd_star_create(sd_star** out, const sd_star_config* cfg, const void* i
     h->cfg = *cfg;
     h->esz = esz;
     h->loop = cfg->transport == SD_STAR_LOOPBACK;
+    h->qm = cfg->payload == SD_STAR_PAYLOAD_QMETA;
+    if (cfg->payload != SD_STAR_PAYLOAD_FULL && cfg->payload != SD_STAR_PAYLOAD_QMETA) {
+        delete h;
+        return fail(SD_ERR_INVALID_ARGUMENT, "payload");
+    }
     h->sched = StarScheduler(cfg->world - 1, cfg->max_shape.k);
     st = star_init(h, ids);
     if (st != SD_OK) {
@@ -556,9 +571,49 @@ static sd_status star_init(sd_star* h, const void* ids) {
         st = alloc_staging(h, cfg->n_slots);
         if (st != SD_OK) return st;
     }
+    if (h->qm && !h->loop) {
+        st = exchange_qstage(h);
+        if (st != SD_OK) return st;
+    }
     SD_CUDA(cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming));
     SD_CUDA(cudaEventCreate(&h->ev_origin));
     SD_CUDA(cudaEventRecord(h->ev_origin, 0));
+    return SD_OK;
+}
+
+// QMETA payload over NCCL: the draft allocates one q staging buffer per (verifier, slot) and sends
+// its CUDA IPC handle to the verifier once (the one-time handshake of P:262-263); the verifier maps
+// it and its sd_verify_qmeta reads the stop rows q_L over NVLink.  Per round only ids + metadata
+// travel through NCCL.
+static sd_status exchange_qstage(sd_star* h) {
+    const sd_star_config* cfg = &h->cfg;
+    const sd_shape& ms = cfg->max_shape;
+    const size_t qbytes = (size_t)ms.batch * ms.k * ms.vocab * h->esz;
+    const size_t hb = sizeof(cudaIpcMemHandle_t) * cfg->n_slots;
+    void* dbuf = nullptr;
+    SD_CUDA(cudaMalloc(&dbuf, hb));
+    std::vector<cudaIpcMemHandle_t> hs(cfg->n_slots);
+    if (cfg->rank == 0) {
+        h->qstage.assign(static_cast<size_t>(cfg->world) * cfg->n_slots, nullptr);
+        for (int v = 1; v < cfg->world; ++v) {
+            for (int s = 0; s < cfg->n_slots; ++s) {
+                void*& q = h->qstage[static_cast<size_t>(v) * cfg->n_slots + s];
+                SD_CUDA(cudaMalloc(&q, qbytes));
+                SD_CUDA(cudaIpcGetMemHandle(&hs[s], q));
+            }
+            SD_CUDA(cudaMemcpy(dbuf, hs.data(), hb, cudaMemcpyHostToDevice));
+            SD_NCCL(ncclSend(dbuf, hb, ncclInt8, 1, h->down[v], h->sdown[v]));
+            SD_CUDA(cudaStreamSynchronize(h->sdown[v]));
+        }
+    } else {
+        SD_NCCL(ncclRecv(dbuf, hb, ncclInt8, 0, h->down[0], h->sdown[0]));
+        SD_CUDA(cudaStreamSynchronize(h->sdown[0]));
+        SD_CUDA(cudaMemcpy(hs.data(), dbuf, hb, cudaMemcpyDeviceToHost));
+        h->qpeer.assign(cfg->n_slots, nullptr);
+        for (int s = 0; s < cfg->n_slots; ++s)
+            SD_CUDA(cudaIpcOpenMemHandle(&h->qpeer[s], hs[s], cudaIpcMemLazyEnablePeerAccess));
+    }
+    SD_CUDA(cudaFree(dbuf));
     return SD_OK;
 }
 
@@ -606,6 +661,8 @@ sd_status sd_star_round(sd_star* h, const sd_round_desc* d, cudaStream_t stream)
         if (v < 1 || v >= h->cfg.world) return fail(SD_ERR_INVALID_ARGUMENT, "verifier");
         if (!d->draft_ids || (!greedy && !d->q_logits))
             return fail(SD_ERR_INVALID_ARGUMENT, "draft_ids / q_logits NULL");
+        if (h->qm && !greedy && !d->q_meta)
+            return fail(SD_ERR_INVALID_ARGUMENT, "QMETA payload: q_meta NULL");
         sd_star::Slot& s = h->slots[static_cast<size_t>(v) * h->cfg.n_slots + d->slot];
         if (s.busy) return fail(SD_ERR_INVALID_ARGUMENT, "slot still in flight");
         SD_CUDA(cudaEventRecord(h->ev_ready, stream));
@@ -617,13 +674,22 @@ sd_status sd_star_round(sd_star* h, const sd_round_desc* d, cudaStream_t stream)
             const size_t i = static_cast<size_t>(v) * h->cfg.n_slots + d->slot;
             cudaStream_t cs = h->sdown[v];
             SD_CUDA(cudaMemcpyAsync(h->ids_buf[i], d->draft_ids, B * k * 4, cudaMemcpyDeviceToDevice, cs));
-            if (!greedy)
+            if (!greedy && h->qm)
+                SD_CUDA(cudaMemcpyAsync(h->qmeta_buf[i], d->q_meta, B * k * sizeof(sd_qmeta),
+                                        cudaMemcpyDeviceToDevice, cs));
+            else if (!greedy)
                 SD_CUDA(cudaMemcpyAsync(h->q_buf[i], d->q_logits, B * k * V * h->esz,
                                         cudaMemcpyDeviceToDevice, cs));
             if (h->cfg.target_ms > 0.0f) SD_CUDA(launch_spin_ns(static_cast<uint64_t>(h->cfg.target_ms * 1e6), cs));
-            sd_status st = sd_verify(d->p_logits, greedy ? nullptr : h->q_buf[i], h->ids_buf[i], &sh,
-                                     h->cfg.temperature, h->cfg.seed, d->round, d->request_id_base,
-                                     h->L_buf[i], h->tok_buf[i], nullptr, h->ws[i], h->ws_bytes, cs);
+            // QMETA: the virtual verifier reads its stop rows straight from the draft's q_logits
+            sd_status st = h->qm && !greedy
+                ? sd_verify_qmeta(d->p_logits, d->q_logits, static_cast<const sd_qmeta*>(h->qmeta_buf[i]),
+                                  h->ids_buf[i], &sh, h->cfg.temperature, h->cfg.seed, d->round,
+                                  d->request_id_base, h->L_buf[i], h->tok_buf[i], nullptr, h->ws[i],
+                                  h->ws_bytes, cs)
+                : sd_verify(d->p_logits, greedy ? nullptr : h->q_buf[i], h->ids_buf[i], &sh,
+                            h->cfg.temperature, h->cfg.seed, d->round, d->request_id_base,
+                            h->L_buf[i], h->tok_buf[i], nullptr, h->ws[i], h->ws_bytes, cs);
             if (st != SD_OK) return st;
             SD_CUDA(cudaEventRecord(h->ev_used[i], cs));
             SD_CUDA(cudaStreamWaitEvent(h->sup[v], h->ev_used[i], 0));
@@ -631,9 +697,16 @@ sd_status sd_star_round(sd_star* h, const sd_round_desc* d, cudaStream_t stream)
             SD_CUDA(cudaMemcpyAsync(d->out_tokens, h->tok_buf[i], B * (k + 1) * 4,
                                     cudaMemcpyDeviceToDevice, h->sup[v]));
         } else {
+            const size_t i = static_cast<size_t>(v) * h->cfg.n_slots + d->slot;
+            if (h->qm && !greedy && d->q_logits != h->qstage[i])   // stop rows are read from here
+                SD_CUDA(cudaMemcpyAsync(h->qstage[i], d->q_logits, B * k * V * h->esz,
+                                        cudaMemcpyDeviceToDevice, h->sdown[v]));
             SD_NCCL(ncclGroupStart());
             SD_NCCL(ncclSend(d->draft_ids, B * k, ncclInt32, 1, h->down[v], h->sdown[v]));
-            if (!greedy) SD_NCCL(ncclSend(d->q_logits, B * k * V, dt, 1, h->down[v], h->sdown[v]));
+            if (!greedy && h->qm)
+                SD_NCCL(ncclSend(d->q_meta, B * k * sizeof(sd_qmeta), ncclInt8, 1, h->down[v], h->sdown[v]));
+            else if (!greedy)
+                SD_NCCL(ncclSend(d->q_logits, B * k * V, dt, 1, h->down[v], h->sdown[v]));
             SD_NCCL(ncclGroupEnd());
             SD_NCCL(ncclGroupStart());
             SD_NCCL(ncclRecv(d->out_accept_len, B, ncclInt32, 1, h->up[v], h->sup[v]));
@@ -656,14 +729,21 @@ sd_status sd_star_round(sd_star* h, const sd_round_desc* d, cudaStream_t stream)
     SD_CUDA(cudaStreamWaitEvent(h->sdown[0], h->ev_used[sl], 0));
     SD_NCCL(ncclGroupStart());
     SD_NCCL(ncclRecv(ids, B * k, ncclInt32, 0, h->down[0], h->sdown[0]));
-    if (!greedy) SD_NCCL(ncclRecv(q, B * k * V, dt, 0, h->down[0], h->sdown[0]));
+    if (!greedy && h->qm)
+        SD_NCCL(ncclRecv(h->qmeta_buf[sl], B * k * sizeof(sd_qmeta), ncclInt8, 0, h->down[0], h->sdown[0]));
+    else if (!greedy)
+        SD_NCCL(ncclRecv(q, B * k * V, dt, 0, h->down[0], h->sdown[0]));
     SD_NCCL(ncclGroupEnd());
     SD_CUDA(cudaEventRecord(h->ev_recv[sl], h->sdown[0]));
     SD_CUDA(cudaStreamWaitEvent(stream, h->ev_recv[sl], 0));
     if (h->cfg.target_ms > 0.0f) SD_CUDA(launch_spin_ns(static_cast<uint64_t>(h->cfg.target_ms * 1e6), stream));
-    sd_status st = sd_verify(d->p_logits, greedy ? nullptr : q, ids, &sh, h->cfg.temperature,
-                             h->cfg.seed, d->round, d->request_id_base, d->out_accept_len,
-                             d->out_tokens, nullptr, h->ws[sl], h->ws_bytes, stream);
+    sd_status st = h->qm && !greedy
+        ? sd_verify_qmeta(d->p_logits, h->qpeer[sl], static_cast<const sd_qmeta*>(h->qmeta_buf[sl]),
+                          ids, &sh, h->cfg.temperature, h->cfg.seed, d->round, d->request_id_base,
+                          d->out_accept_len, d->out_tokens, nullptr, h->ws[sl], h->ws_bytes, stream)
+        : sd_verify(d->p_logits, greedy ? nullptr : q, ids, &sh, h->cfg.temperature, h->cfg.seed,
+                    d->round, d->request_id_base, d->out_accept_len, d->out_tokens, nullptr,
+                    h->ws[sl], h->ws_bytes, stream);
     if (st != SD_OK) return st;
     SD_CUDA(cudaEventRecord(h->ev_used[sl], stream));
     SD_CUDA(cudaStreamWaitEvent(h->sup[0], h->ev_used[sl], 0));
@@ -829,6 +909,11 @@ sd_status sd_star_destroy(sd_star* h) {
     for (auto i : h->L_buf) cudaFree(i);
     for (auto i : h->tok_buf) cudaFree(i);
     for (auto w : h->ws) cudaFree(w);
+    for (auto p : h->qpeer)
+        if (p) cudaIpcCloseMemHandle(p);
+    for (auto p : h->qstage)
+        if (p) cudaFree(p);
+    for (auto p : h->qmeta_buf) cudaFree(p);
     if (h->ev_ready) cudaEventDestroy(h->ev_ready);
     if (h->ev_origin) cudaEventDestroy(h->ev_origin);
     delete h;

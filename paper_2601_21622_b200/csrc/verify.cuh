@@ -41,6 +41,17 @@ struct RowStat {
     int32_t argmax;      // greedy: argmax of p row (lowest index)
 };
 
+// Per (request b, position j) draft-row metadata (NEXT-1 / NEXT-2; include/starsd.h sd_qmeta):
+// the draft row's statistics in the verify kernels' own arithmetic, so a verify that reads them
+// instead of the q row takes bit-identical decisions.
+struct QMeta {
+    double S;            // sum of 2^(z c2 - D) over the row
+    float D;             // scaled row max (greedy: raw max)
+    float zx;            // z(x_j)
+    int32_t status;      // kNonfinite / kEmptyRow of the q row
+    int32_t reserved;
+};
+
 // Per (request b, chunk c) of the sampling pass.
 struct PartB {
     double R;            // residual mass of the slice (or p mass at the bonus position)
@@ -91,6 +102,8 @@ struct Params {
     int32_t chain;               // k_row_stats launched as a programmatic dependent of whatever
                                  // kernel precedes it on the stream (griddepcontrol.wait first)
     int32_t esz;                 // bytes per logit
+    const QMeta* qmeta;          // [B][k] draft-row metadata: the q rows are then read only at the
+                                 // stop position (sd_verify_qmeta); NULL: full q rows
 };
 
 // k_row_stats cluster size for a row of nch chunks: a cluster covers the whole row when nch <= 8

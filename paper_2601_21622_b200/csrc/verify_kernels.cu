@@ -371,10 +371,19 @@ __device__ __forceinline__ PartA comb_as_part(const Comb& C) {
 // row statistics go to rowstat, then "decided" (and "stopped") bits are ORed into the request's
 // state with release semantics, so a CTA that sees the request settled also sees its rowstat.
 template <bool GREEDY>
-__device__ __forceinline__ void decide(const Params& P, int b, int j, int x, const Comb& C) {
+__device__ __forceinline__ void decide(const Params& P, int b, int j, int x, const Comb& Cin) {
     const int kk = P.k;
     const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
     const bool load_q = !GREEDY && j < kk;
+    Comb C = Cin;
+    int32_t qst = 0;
+    if (load_q && P.qmeta) {   // lazy q (NEXT-1): the draft's row statistics replace q's partials
+        const QMeta m = P.qmeta[static_cast<size_t>(b) * kk + j];
+        C.RMq = m.D;
+        C.RSq = m.S;
+        C.zxq = m.zx;
+        qst = m.status & (kNonfinite | kEmptyRow);
+    }
     int32_t st = 0;
     bool stop = false;
     double a = NAN;
@@ -385,7 +394,7 @@ __device__ __forceinline__ void decide(const Params& P, int b, int j, int x, con
         else if (C.RMp == -INFINITY) st = kEmptyRow;
     }
     if (!st && load_q) {
-        if (C.flags & kPartNonfiniteQ) st = kNonfinite;
+        if ((C.flags & kPartNonfiniteQ) || (qst & kNonfinite)) st = kNonfinite;
         else if (C.RMq == -INFINITY) st = kEmptyRow;
     }
     if (st) {
@@ -975,7 +984,7 @@ __global__ void __launch_bounds__(kThreads, GREEDY ? 8 : 6) k_row_stats(const Pa
 
     const int c0 = c * P.CH;
     const int len = max(0, min(P.CH, P.V - c0));   // CL > 1: empty padding chunks past V
-    const bool load_q = !GREEDY && j < kk;
+    const bool load_q = !GREEDY && j < kk && P.qmeta == nullptr;   // (lazy q: metadata instead)
     const E* gp = static_cast<const E*>(P.p) + static_cast<int64_t>(pos) * P.ld_p + c0;
     const E* gq = load_q ? static_cast<const E*>(P.q) +
                                (static_cast<int64_t>(b) * kk + j) * P.ld_q + c0
@@ -1594,6 +1603,38 @@ __global__ void k_trace(const RowStat* rowstat, const double* rres, const int32_
 }
 
 // ------------------------------------------------------------------------------------------
+// Row statistics only (sd_draft_qmeta): the second kernel just resets the workspace words.
+__global__ void k_reset(const Params P) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (P.tagpub && threadIdx.x == 0 && blockIdx.x == 0)
+        P.epoch[0] += 1u;   // k_row_stats is complete: the next call tags with a new value
+    if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= P.B) return;
+    if (P.out_status) P.out_status[b] = P.rowstat[static_cast<size_t>(b) * (P.k + 1)].status;
+    P.state[b] = 0ull;
+    for (int i = 0; i <= P.k; ++i) P.ticketA[static_cast<size_t>(b) * (P.k + 1) + i] = 0u;
+}
+
+// Draft-row metadata (NEXT-1/2): row r's statistics (k = 0 calls: one row per "request") and the
+// logit of its token ids[r].
+template <typename E>
+__global__ void k_qmeta(const Params P, const int32_t* ids, QMeta* out) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= P.B) return;
+    const RowStat rs = P.rowstat[r];
+    const int x = ids[r];
+    QMeta m;
+    m.S = rs.S_p;
+    m.D = rs.M_p;
+    m.zx = (x >= 0 && x < P.V) ? Elt<E>::one(static_cast<const E*>(P.p) + static_cast<int64_t>(r) * P.ld_p, x)
+                               : NAN;
+    m.status = rs.status & (kNonfinite | kEmptyRow);
+    m.reserved = 0;
+    out[r] = m;
+}
+
+// ------------------------------------------------------------------------------------------
 __global__ void k_philox(uint64_t seed, uint64_t round, const uint32_t* pos, const uint64_t* rid,
                          int n, uint32_t* out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1725,6 +1766,8 @@ static cudaError_t launch_greedy(const Params& P, cudaStream_t st, cudaEvent_t e
     return launch_dependent(k_finalize_greedy, dim3((P.B + 127) / 128), 128, 0, st, P);
 }
 
+cudaError_t qmeta_gather(const Params& P, bool bf16, const int32_t* ids, QMeta* out,
+                         cudaStream_t st);
 cudaError_t launch_verify(const Params& P, bool greedy, bool bf16, cudaStream_t st,
                           cudaEvent_t ev0, cudaEvent_t ev1) {
     if (greedy)
@@ -1732,6 +1775,25 @@ cudaError_t launch_verify(const Params& P, bool greedy, bool bf16, cudaStream_t 
                     : launch_greedy<float>(P, st, ev0, ev1);
     return bf16 ? launch_sampled<__nv_bfloat16>(P, st, ev0, ev1)
                 : launch_sampled<float>(P, st, ev0, ev1);
+}
+
+// Row statistics of B rows (P.k == 0) without sampling, then the metadata gather.
+cudaError_t launch_qmeta(const Params& P, bool bf16, const int32_t* ids, QMeta* out,
+                         cudaStream_t st) {
+    if (bf16) launch_stats<__nv_bfloat16, false>(P, st);
+    else launch_stats<float, false>(P, st);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = launch_dependent(k_reset, dim3((P.B + 127) / 128), 128, 0, st, P);
+    if (e != cudaSuccess) return e;
+    return qmeta_gather(P, bf16, ids, out, st);
+}
+cudaError_t qmeta_gather(const Params& P, bool bf16, const int32_t* ids, QMeta* out,
+                         cudaStream_t st) {
+    if (P.B == 0) return cudaSuccess;
+    if (bf16) k_qmeta<__nv_bfloat16><<<(P.B + 127) / 128, 128, 0, st>>>(P, ids, out);
+    else k_qmeta<float><<<(P.B + 127) / 128, 128, 0, st>>>(P, ids, out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_trace(const Params& P, const int32_t* accept_len, double* lam_p, double* lam_q,

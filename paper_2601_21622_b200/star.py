@@ -168,7 +168,8 @@ class Star:
     def __init__(self, rank: int, world: int, max_batch: int, k: int, vocab: int,
                  temperature: float, seed: int = 0, n_slots: int = 2,
                  dtype: torch.dtype = torch.float32, device=None, ids: bytes | None = None,
-                 transport: str = "nccl", timeout_ms: int = 60000, target_ms: float = 0.0):
+                 transport: str = "nccl", timeout_ms: int = 60000, target_ms: float = 0.0,
+                 payload: str = "full"):
         dev = torch.device(device if device is not None else "cuda")
         if dev.type != "cuda":
             raise StarsdError("Star needs a CUDA device")
@@ -181,7 +182,8 @@ class Star:
                               _lib.Shape(max_batch, k, vocab, vocab, vocab, _dt(dtype)),
                               self.temperature, seed, timeout_ms,
                               dev.index if dev.index is not None else torch.cuda.current_device(),
-                              tcode, float(target_ms))
+                              tcode, float(target_ms),
+                              {"full": _lib.SD_STAR_PAYLOAD_FULL, "qmeta": _lib.SD_STAR_PAYLOAD_QMETA}[payload])
         self._h = ctypes.c_void_p()
         idbuf = None if ids is None else ctypes.create_string_buffer(ids, len(ids))
         check(self._L.sd_star_create(ctypes.byref(self._h), ctypes.byref(cfg), idbuf),
@@ -193,11 +195,14 @@ class Star:
 
     def submit(self, verifier: int, slot: int, round: int, ids: torch.Tensor,
                q: torch.Tensor | None, accept_len: torch.Tensor, tokens: torch.Tensor,
-               request_id_base: int = 0, p: torch.Tensor | None = None, stream=None):
-        """Draft: send (ids [B,k], q [B,k,V]) to `verifier` for `slot` and post the receive of
-        (accept_len [B], tokens [B,k+1]).  Returns immediately; completion shows up in poll()."""
+               request_id_base: int = 0, p: torch.Tensor | None = None, stream=None,
+               qmeta: torch.Tensor | None = None):
+        """Draft: send (ids [B,k], q [B,k,V]) -- or, with payload="qmeta", ids + qmeta [B,k,3]
+        (sd_qmeta records from draft_sample / draft_qmeta; q must then stay valid until the round
+        returns) -- to `verifier` for `slot` and post the receive of (accept_len [B],
+        tokens [B,k+1]).  Returns immediately; completion shows up in poll()."""
         d = _lib.RoundDesc(verifier, slot, round, ids.shape[0], request_id_base, _ptr(p),
-                           _ptr(ids), _ptr(q), _ptr(accept_len), _ptr(tokens))
+                           _ptr(ids), _ptr(q), _ptr(accept_len), _ptr(tokens), _ptr(qmeta))
         check(self._L.sd_star_round(self._h, ctypes.byref(d), self._stream(stream)),
               "sd_star_round")
 
@@ -206,7 +211,7 @@ class Star:
               stream=None):
         """Verifier: receive the round's (ids, q), verify against p [B,k+1,V], send results."""
         d = _lib.RoundDesc(self.rank, slot, round, batch, request_id_base, _ptr(p), None, None,
-                           _ptr(accept_len), _ptr(tokens))
+                           _ptr(accept_len), _ptr(tokens), None)
         check(self._L.sd_star_round(self._h, ctypes.byref(d), self._stream(stream)),
               "sd_star_round")
 
@@ -256,3 +261,111 @@ class Star:
             self.close()
         except Exception:
             pass
+
+
+def simulate_trace(trace: dict, service_ms: float, return_ms: float, beta, k: int,
+                   n_slots: int = 2, max_active: int = 128, seed: int = 0,
+                   window_ms: float = 1000.0, until_ms: float | None = None) -> dict:
+    """Trace-driven star (BASELINE config 5, bursty arrivals): the draft's FIFO scheduler (the same
+    sd_sched_* the NCCL star runs) serves rounds of per-verifier cohorts whose membership follows
+    the request trace.  trace: {v: [(arrival_ms, length_tokens), ...]} (workload.bursty_trace).
+    A verifier keeps <= max_active requests in n_slots cohorts; a cohort with at least one active
+    request issues its next round when its previous one returned (closed loop); a round costs
+    the draft service_ms (S(d), Eq. 5, independent of the batch) and returns return_ms later
+    (Z(d), Eq. 6); each request emits L + 1 tokens per round, L ~ truncated geometric with per-
+    verifier acceptance beta[v-1] (Lemma 1, i.i.d. acceptance).  Returns the busy fraction overall
+    and per window, per-verifier tokens/s, mean T_wait and completed requests.  Runs until every
+    request completed, or until the draft clock reaches until_ms."""
+    import heapq
+
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    nv = len(trace)
+    beta = np.broadcast_to(np.asarray(beta, np.float64), (nv,))
+    sched = Scheduler(nv, k)
+    arrivals = {v: list(trace[v]) for v in trace}
+    nxt = {v: 0 for v in trace}
+    active = {(v, s): [] for v in trace for s in range(n_slots)}     # [remaining, length]
+    count = {v: 0 for v in trace}
+    waiting_stream = {(v, s): True for v in trace for s in range(n_slots)}  # no round in flight
+    tokens = np.zeros(nv)
+    done_req = 0
+    events = []        # (t, kind, v, s): kind 0 = return, 1 = arrival wake-up
+    for v in trace:
+        if arrivals[v]:
+            heapq.heappush(events, (arrivals[v][0][0], 1, v, -1))
+    t = 0.0
+    busy = []
+    last_t = max((r[-1][0] for r in arrivals.values() if r), default=0.0)
+
+    def admit(v, now):
+        while nxt[v] < len(arrivals[v]) and arrivals[v][nxt[v]][0] <= now and count[v] < max_active:
+            ln = arrivals[v][nxt[v]][1]
+            s = nxt[v] % n_slots
+            active[(v, s)].append([ln, ln])
+            count[v] += 1
+            nxt[v] += 1
+
+    def ready(v, now):
+        for s in range(n_slots):
+            if waiting_stream[(v, s)] and active[(v, s)]:
+                waiting_stream[(v, s)] = False
+                sched.push(v, s, 0, now)
+        if nxt[v] < len(arrivals[v]) and count[v] < max_active:
+            heapq.heappush(events, (max(now, arrivals[v][nxt[v]][0]), 1, v, -1))
+
+    while True:
+        # move every event due by t into the queue
+        while events and events[0][0] <= t:
+            te, kind, v, s = heapq.heappop(events)
+            if kind == 0:                                   # a round of (v, s) returned
+                reqs = active[(v, s)]
+                L = np.minimum(rng.geometric(1.0 - beta[v - 1], len(reqs)) - 1, k) \
+                    if beta[v - 1] < 1.0 else np.full(len(reqs), k)
+                keep = []
+                for rq, l in zip(reqs, L):
+                    emit = min(int(l) + 1, rq[0])
+                    tokens[v - 1] += emit
+                    rq[0] -= emit
+                    if rq[0] > 0:
+                        keep.append(rq)
+                    else:
+                        done_req += 1
+                        count[v] -= 1
+                active[(v, s)] = keep
+                waiting_stream[(v, s)] = True
+                sched.observe(v, return_ms, L.astype(np.int32))
+            admit(v, te)
+            ready(v, te)
+        if until_ms is not None and t >= until_ms:
+            break
+        got = sched.pop(t)
+        if got is None:
+            if not events:
+                break
+            t = events[0][0]                                # the draft idles (T_idle)
+            continue
+        v, s, _ = got
+        sched.service(v, t, t + service_ms)
+        busy.append((t, t + service_ms))
+        t += service_ms
+        heapq.heappush(events, (t + return_ms, 0, v, s))
+        if t > last_t + 1e6:
+            break
+    st = sched.stats()
+    horizon = max(b[1] for b in busy) if busy else 0.0
+    nw = int(np.ceil(horizon / window_ms)) if horizon > 0 else 0
+    per_win = np.zeros(nw)
+    for a, b in busy:
+        w0, w1 = int(a // window_ms), int(min(b, horizon - 1e-9) // window_ms)
+        for w in range(w0, w1 + 1):
+            lo, hi = max(a, w * window_ms), min(b, (w + 1) * window_ms)
+            if hi > lo:
+                per_win[w] += hi - lo
+    out = {"busy_fraction": float(sum(b - a for a, b in busy) / horizon) if horizon else 0.0,
+           "busy_per_window": (per_win / window_ms).tolist(),
+           "tokens_per_s": (tokens / (horizon / 1000.0)).tolist() if horizon else [0.0] * nv,
+           "mean_wait_ms": st["mean_wait_ms"], "rounds": st["rounds"],
+           "completed_requests": done_req, "horizon_ms": horizon}
+    sched.close()
+    return out

@@ -199,3 +199,49 @@ def test_verify_zero_residual_samples_from_p():
         else:
             assert L[b] == 1 and not st[b] & oracle.FAULT_ZERO_RESIDUAL
     assert rej > 300
+
+
+# ---------------------------------------------------------------- draft sampler (NEXT-2) ---
+def test_draft_sampler_hand_cdf_and_counter_domain():
+    """sd_ref_draft_sample on the hand row q = [.1,.2,.3,.4]: x = the first y whose hand CDF
+    (.1,.3,.6,1) exceeds u = u24(w1) of the Philox counter (0, round, 2^63 + (rid_base + b) k + j)
+    (reading D-1), and log q(x) = log of the hand probability; k = 3 positions share the
+    row but use their own counters."""
+    ex = WORKED["inverse_cdf_hand"]
+    B, k = 300, 3
+    q = np.broadcast_to(logits(ex["p0"]), (B, k, 4)).copy()
+    ids, logq, mu, st = oracle.draft_sample(q, 1.0, seed=21, round=6, rid_base=40)
+    cdf = np.asarray(ex["bonus_cdf"])
+    for b in range(B):
+        for j in range(k):
+            _, u = oracle.uniforms(21, 0, 6, (1 << 63) + (40 + b) * k + j)
+            if np.min(np.abs(cdf - u)) < 1e-6:
+                continue
+            x = int(np.argmax(cdf > u))
+            assert ids[b, j] == x and abs(logq[b, j] - np.log(ex["p0"][x])) < TOL
+    assert np.all(st == 0)
+
+
+def test_draft_sampler_follows_the_library_softmax():
+    """20000 draws from one V = 50 row at T = 0.7: the histogram matches scipy's softmax(z/T)
+    (G-test), greedy (T = 0) is numpy's argmax with the lowest index on ties, faulty rows give -1."""
+    from scipy import stats
+    rng = np.random.default_rng(8)
+    z = rng.normal(0, 1.5, 50).astype(np.float32)
+    q = np.broadcast_to(z, (20000, 1, 50)).copy()
+    ids, logq, mu, st = oracle.draft_sample(q, 0.7, seed=3, round=1)
+    pr = special.softmax(z.astype(np.float64) / 0.7)
+    obs = np.bincount(ids[:, 0], minlength=50)
+    keep = pr * 20000 > 5
+    g = 2 * np.sum(obs[keep] * np.log(np.maximum(obs[keep], 1) / (20000 * pr[keep])))
+    assert stats.chi2.sf(g, keep.sum() - 1) > 1e-4
+    np.testing.assert_allclose(logq[:, 0], np.log(pr[ids[:, 0]]), atol=1e-9)
+    zt = z.copy()
+    zt[[7, 30]] = zt.max() + 1.0                      # a tie for the maximum: lowest index wins
+    g0 = oracle.draft_sample(zt[None, None].copy(), 0.0)[0]
+    assert g0[0, 0] == int(np.argmax(zt)) == 7
+    bad = np.stack([z, z]).copy()[None]
+    bad[0, 0, 3] = np.nan
+    bad[0, 1, :] = -np.inf
+    ids, _, _, st = oracle.draft_sample(bad, 1.0)
+    assert list(ids[0]) == [-1, -1] and list(st[0]) == [oracle.FAULT_NONFINITE, oracle.FAULT_EMPTY_ROW]

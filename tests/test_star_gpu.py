@@ -21,11 +21,15 @@ def _dev(a):
     return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
 
 
-@pytest.mark.parametrize("T", [1.0, 0.0])
-def test_loopback_rounds_match_oracle_in_fifo_order(T):
+@pytest.mark.parametrize("T,payload", [(1.0, "full"), (0.0, "full"), (1.0, "qmeta")])
+def test_loopback_rounds_match_oracle_in_fifo_order(T, payload):
+    """payload="qmeta" (NEXT-1): only ids + 24-byte metadata per draft token go out; the virtual
+    verifier reads its stop rows from the draft's q rows (sd_verify_qmeta)."""
+    import paper_2601_21622_b200 as sd
     N, slots, rounds_per_stream, B, k, V = 3, 2, 4, 24, 4, 3000
     seed = 77
-    h = star.Star(0, N + 1, B, k, V, T, seed=seed, n_slots=slots, device=DEV, transport="loopback")
+    h = star.Star(0, N + 1, B, k, V, T, seed=seed, n_slots=slots, device=DEV, transport="loopback",
+                  payload=payload)
     inflight, done = {}, []
 
     def submit(v, s, r):
@@ -34,7 +38,10 @@ def test_loopback_rounds_match_oracle_in_fifo_order(T):
              "L": torch.full((B,), -7, dtype=torch.int32, device=DEV),
              "tok": torch.full((B, k + 1), -7, dtype=torch.int32, device=DEV)}
         rid = (v << 40) + (s << 20)
-        h.submit(v, s, r, t["ids"], t["q"], t["L"], t["tok"], request_id_base=rid, p=t["p"])
+        qm = sd.draft_qmeta(t["q"], t["ids"], T) if payload == "qmeta" else None
+        t["qm"] = qm
+        h.submit(v, s, r, t["ids"], t["q"], t["L"], t["tok"], request_id_base=rid, p=t["p"],
+                 qmeta=qm)
         inflight[(v, s)] = (r, d, t, rid)
 
     for s in range(slots):
@@ -100,3 +107,46 @@ def test_loopback_busy_fraction_follows_sec41_closed_form(N):
     pred = star.predicted(N, S, Z)
     assert st["rounds"] == 20 * N
     assert abs(st["busy_fraction"] - pred["busy_fraction"]) < 0.08, (st, pred)
+
+
+def test_loopback_varying_batch_per_slot_and_online_predictor():
+    """ADVICE r1 (high): a slot's rounds may carry different batch sizes (B_v <= max_shape.batch);
+    the slot's verify workspace must re-zero itself when the layout changes.  Rounds alternate
+    B = 8, 24, 3, 24 on the same slots and every result matches the oracle.  The online predictor
+    then reports S(d), Z(d) > 0 and a beta estimate from the observed accept lengths."""
+    N, slots, B_max, k, V, T = 2, 2, 24, 4, 3000, 1.0
+    h = star.Star(0, N + 1, B_max, k, V, T, seed=5, n_slots=slots, device=DEV, transport="loopback")
+    sizes = [8, 24, 3, 24]
+    inflight = {}
+
+    def submit(v, s, r):
+        B = sizes[r % len(sizes)]
+        d = make_batch(V, k, B, T, 30.0, seed=500 * v + 50 * s + r)
+        t = {"p": _dev(d["p"]), "q": _dev(d["q"]), "ids": _dev(d["ids"]),
+             "L": torch.full((B,), -7, dtype=torch.int32, device=DEV),
+             "tok": torch.full((B, k + 1), -7, dtype=torch.int32, device=DEV)}
+        h.draft_begin(verifier=v)
+        h.submit(v, s, r, t["ids"], t["q"], t["L"], t["tok"], request_id_base=r * 100, p=t["p"])
+        h.draft_end()
+        inflight[(v, s)] = (r, d, t)
+
+    for s in range(slots):
+        for v in range(1, N + 1):
+            submit(v, s, 0)
+    n = 0
+    while inflight:
+        got = h.poll(timeout_us=10_000_000)
+        assert got is not None
+        v, s, r = got
+        r0, d, t = inflight.pop((v, s))
+        L, tok = t["L"].cpu().numpy(), t["tok"].cpu().numpy()
+        ref = oracle.verify(d["p"], d["q"], d["ids"], T, seed=5, round=r, rid_base=r * 100, trace=True)
+        compare(d, (L, tok, np.zeros(len(L), np.int32)), ref, T, 5, r, r * 100)
+        h.observe(v, L)
+        n += 1
+        if r + 1 < 8:
+            submit(v, s, r + 1)
+    assert n == N * slots * 8
+    pr = h.predict(0.01)
+    assert pr["service_ms"] > 0 and pr["return_ms"] > 0 and 0 < pr["expected_accepted"] < N * k
+    h.close()

@@ -12,3 +12,6 @@ timeout 600 python bench.py --config c2 --no-cpu > gpurun_out/bench_c2.json 2> g
 timeout 600 python bench.py --config c3g --no-cpu --no-e2e > gpurun_out/bench_c3g.json 2> gpurun_out/bench_c3g.err
 tail -3 gpurun_out/pytest_gpu.log
 cat gpurun_out/bench_c3.json gpurun_out/bench_c2.json gpurun_out/bench_c3g.json | cut -c1-600
+timeout 600 python bench.py --star-loopback 3 --steps 10 --warmup 3 > gpurun_out/bench_star_loop.json 2> gpurun_out/bench_star_loop.err
+timeout 600 python bench.py --star-loopback 3 --steps 10 --warmup 3 --payload qmeta > gpurun_out/bench_star_loop_qm.json 2> gpurun_out/bench_star_loop_qm.err
+tail -c 1500 gpurun_out/bench_star_loop.json; tail -5 gpurun_out/bench_star_loop.err

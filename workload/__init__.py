@@ -14,6 +14,7 @@ workloads (DESIGN.md "Input recipe"):
 """
 from .synth import (CONFIGS, make_batch, make_batch_torch, make_tiny_tables, tiny_batch,
                     bf16_bits, log_dirichlet)
+from .trace import C4_BATCH, C4_KAPPA, bursty_trace
 
 __all__ = ["CONFIGS", "make_batch", "make_batch_torch", "make_tiny_tables", "tiny_batch",
-           "bf16_bits", "log_dirichlet"]
+           "bf16_bits", "log_dirichlet", "bursty_trace", "C4_BATCH", "C4_KAPPA"]
