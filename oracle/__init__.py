@@ -77,6 +77,12 @@ def lib():
         L.sd_ref_draft_sample.argtypes = [vp, i32, i32, i32, i64, i32, dbl, u64, u64, u64, vp, vp,
                                           vp, vp]
         L.sd_ref_draft_sample.restype = ctypes.c_int
+        L.sd_ref_tree_verify.argtypes = [vp, vp, vp, i32, i32, i32, i32, i64, i64, i32, dbl, u64,
+                                         u64, u64, vp, vp, vp, vp, vp]
+        L.sd_ref_tree_verify.restype = ctypes.c_int
+        L.sd_ref_tree_outcome_dist.argtypes = [vp, vp, vp, i32, i32, i32, i32, i64, i64, i32, dbl,
+                                               vp]
+        L.sd_ref_tree_outcome_dist.restype = ctypes.c_int
         L.sd_ref_beta.argtypes = [vp, vp, i32, dbl]
         L.sd_ref_beta.restype = dbl
         L.sd_ref_softmax.argtypes = [vp, i32, dbl, vp]
@@ -201,6 +207,52 @@ def draft_sample(q, T, seed=0, round=0, rid_base=0, V=None):
     if rc != 0:
         raise ValueError("sd_ref_draft_sample: invalid argument")
     return ids, logq, mu, st
+
+
+def tree_nodes(m, d):
+    """(N, N_internal) of a full m-ary tree of depth d."""
+    N = sum(m ** t for t in range(d + 1))
+    return N, N - m ** d
+
+
+def tree_verify(p, q, tok, m, d, T, seed=0, round=0, rid_base=0, V=None):
+    """sd_ref_tree_verify: p [B, N, ld], q [B, N_int, ld] (None at T == 0), tok [B, N] int32.
+    Returns (L [B], tokens [B, d+1], status [B], stop node [B], margin mu [B])."""
+    p = np.ascontiguousarray(p)
+    dtype = 1 if p.dtype == np.uint16 else 0
+    if dtype == 0:
+        p = np.ascontiguousarray(p, np.float32)
+    if q is not None:
+        q = np.ascontiguousarray(q, p.dtype)
+    tok = np.ascontiguousarray(tok, np.int32)
+    B, N, ld = p.shape
+    V = ld if V is None else V
+    L = np.zeros(B, np.int32)
+    toks = np.zeros((B, d + 1), np.int32)
+    st = np.zeros(B, np.int32)
+    node = np.zeros(B, np.int32)
+    mu = np.zeros(B, np.float64)
+    rc = lib().sd_ref_tree_verify(_ptr(p), _ptr(q), _ptr(tok), B, m, d, V, ld,
+                                  q.shape[-1] if q is not None else ld, dtype, float(T),
+                                  seed & (2**64 - 1), round & (2**64 - 1), rid_base & (2**64 - 1),
+                                  _ptr(L), _ptr(toks), _ptr(st), _ptr(node), _ptr(mu))
+    if rc != 0:
+        raise ValueError("sd_ref_tree_verify: invalid argument")
+    return L, toks, st, node, mu
+
+
+def tree_outcome_dist(p, q, tok, m, d, T):
+    """sd_ref_tree_outcome_dist: [B, N, V] exact Pr(stop at node n, emit y)."""
+    p = np.ascontiguousarray(p, np.float32)
+    q = np.ascontiguousarray(q, np.float32)
+    tok = np.ascontiguousarray(tok, np.int32)
+    B, N, V = p.shape
+    out = np.zeros((B, N, V), np.float64)
+    rc = lib().sd_ref_tree_outcome_dist(_ptr(p), _ptr(q), _ptr(tok), B, m, d, V, V, V, 0,
+                                        float(T), _ptr(out))
+    if rc != 0:
+        raise ValueError("sd_ref_tree_outcome_dist: invalid argument")
+    return out
 
 
 def beta(zp, zq, T=1.0):

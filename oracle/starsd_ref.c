@@ -555,3 +555,226 @@ int sd_ref_draft_sample(const void* q, int32_t B, int32_t k, int32_t V, int64_t 
     free(buf);
     return 0;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * Lossless tree verification.  The paper drafts a depth-d tree with
+ * branching factor k (Alg. 2) and verifies its k^d paths independently,
+ * keeping the longest accepted one -- a rule that is not lossless (SPEC S:176,
+ * SURVEY C-14).  The replacement (reading D-2 of DESIGN.md) is recursive rejection sampling over
+ * the children of each node (SpecInfer's multi-candidate speculative sampling, the paper's ref.
+ * [miao2024specinfer]): the children c_1..c_m of a node are i.i.d. draws from the node's
+ * draft distribution q; with d_0 = p (the node's target distribution):
+ *   for i = 1..m: accept c_i iff u_i < min(1, d_{i-1}(x_i) / q(x_i)) (x_i = token of c_i) ->
+ *                 descend into c_i;
+ *                 else d_i = norm(max(0, d_{i-1} - q))   (the residual of P:736, applied again)
+ *   all m rejected: emit t ~ d_m and stop;  a leaf reached (depth d): emit the bonus t ~ p_leaf.
+ * m = 1 is exactly the chain of sd_ref_verify (same counters).  Layout: a full m-ary tree of
+ * depth d per request, level order: node 0 = root, children of n are m n + 1 .. m n + m;
+ * N = sum_{t<=d} m^t nodes, N_int = sum_{t<d} m^t internal ones.
+ *   p: [B][N][ld_p] target logits at every node; q: [B][N_int][ld_q] draft logits at internal
+ *   nodes; tok: [B][N] int32 token of each node (root entry unused).
+ * Uniforms (C-8 counters, key = seed): candidate i (0-based) at depth t: u_acc = u24(w0) of
+ * counter (t + 32 i, round, rid); the final sample at depth t: u_smp = u24(w1) of (t, round, rid).
+ * Outputs: out_L[b] = depth reached (accepted tokens), out_tokens[b][0..d] = the accepted path's
+ * tokens, then the emitted token, then -1; out_node[b] (nullable) = the node the walk stopped at;
+ * out_mu[b] (nullable) = the smallest decision margin (|u - a| over the tests decided with a
+ * uniform, and the CDF-cell margin of the final sample relative to its mass), for the tie rule.
+ * T == 0: greedy -- descend into the first child whose token is argmax p_node, else emit argmax.
+ * Hard faults (C-12) on a reached row: L = 0, tokens -1, status bit set.
+ * ---------------------------------------------------------------------------------------- */
+typedef struct {
+    const void* p; const void* q; const int32_t* tok;
+    int32_t m, d, V, N, Nint; int64_t ld_p, ld_q; int32_t dtype; double T;
+    uint64_t seed, round, rid_base;
+} tree_t;
+
+static row_t tree_p(const tree_t* a, int32_t b, int32_t n) {
+    size_t esz = a->dtype == 0 ? 4 : 2;
+    row_t r = {(const char*)a->p + ((size_t)b * a->N + n) * a->ld_p * esz, a->dtype, a->V};
+    return r;
+}
+static row_t tree_q(const tree_t* a, int32_t b, int32_t n) {
+    size_t esz = a->dtype == 0 ? 4 : 2;
+    row_t r = {(const char*)a->q + ((size_t)b * a->Nint + n) * a->ld_q * esz, a->dtype, a->V};
+    return r;
+}
+
+/* d_i of the node into buf (normalised), from d_{i-1} in buf and q (probabilities in qb):
+ * returns the mass R_i = sum max(0, d_{i-1} - q) before normalising (0: keep d_{i-1}, C-6). */
+static double residual_step(double* buf, const double* qb, int32_t V) {
+    double R = 0.0;
+    for (int32_t y = 0; y < V; ++y) {
+        double dd = buf[y] - qb[y];
+        R += dd > 0.0 ? dd : 0.0;
+    }
+    if (!(R > 0.0)) return 0.0;
+    for (int32_t y = 0; y < V; ++y) {
+        double dd = buf[y] - qb[y];
+        buf[y] = (dd > 0.0 ? dd : 0.0) / R;
+    }
+    return R;
+}
+
+static int tree_one(const tree_t* a, int32_t b, int32_t* out_L, int32_t* tokens, int32_t* node_out,
+                    double* mu_out, double* pb, double* qb, double* outc) {
+    const int32_t m = a->m, d = a->d, V = a->V;
+    uint64_t rid = a->rid_base + (uint64_t)b;
+    double mu = 1.0;
+    int32_t n = 0, depth = 0, status = 0;
+    for (int32_t i = 0; i <= d; ++i) tokens[i] = -1;
+    while (1) {
+        row_t pr = tree_p(a, b, n);
+        int f = row_fault(pr);
+        if (f) { status = f; break; }
+        if (depth == d) {                                   /* leaf: bonus t ~ p_leaf (C-3) */
+            if (a->T == 0.0) { tokens[depth] = row_argmax(pr); break; }
+            double lam = row_logsumexp(pr, a->T), R = 0.0;
+            for (int32_t y = 0; y < V; ++y) { pb[y] = prob_of(pr, y, a->T, lam); R += pb[y]; }
+            double us, Cp, Ct;
+            sd_ref_uniforms(a->seed, (uint32_t)depth, a->round, rid, NULL, &us);
+            double th = us * R;
+            tokens[depth] = inverse_cdf(pb, V, th, &Cp, &Ct);
+            double m1 = th - Cp, m2 = Ct - th, ms = (m1 < m2 ? m1 : m2) / R;
+            if (ms < mu) mu = ms;
+            break;
+        }
+        if (a->T == 0.0) {                                  /* greedy tree */
+            int32_t g = row_argmax(pr), next = -1;
+            for (int32_t i = 0; i < m; ++i) {
+                int32_t c = m * n + 1 + i, x = a->tok[(size_t)b * a->N + c];
+                if (x < 0 || x >= V) { status = SD_REF_FAULT_BAD_DRAFT_ID; break; }
+                if (x == g) { next = c; break; }
+            }
+            if (status) break;
+            if (next < 0) { tokens[depth] = g; break; }
+            tokens[depth] = g;
+            n = next;
+            ++depth;
+            continue;
+        }
+        row_t qr = tree_q(a, b, n);
+        f = row_fault(qr);
+        if (f) { status = f; break; }
+        double lp = row_logsumexp(pr, a->T), lq = row_logsumexp(qr, a->T);
+        for (int32_t y = 0; y < V; ++y) { pb[y] = prob_of(pr, y, a->T, lp); qb[y] = prob_of(qr, y, a->T, lq); }
+        int32_t next = -1;
+        for (int32_t i = 0; i < m; ++i) {
+            int32_t c = m * n + 1 + i, x = a->tok[(size_t)b * a->N + c];
+            if (x < 0 || x >= V) { status = SD_REF_FAULT_BAD_DRAFT_ID; break; }
+            if (i > 0 && residual_step(pb, qb, V) == 0.0) status |= SD_REF_FAULT_ZERO_RESIDUAL;
+            double u, acc;
+            if (!(qb[x] > 0.0)) { acc = 0.0; }               /* C-7: q(x) = 0 rejects */
+            else acc = pb[x] >= qb[x] ? 1.0 : pb[x] / qb[x];
+            sd_ref_uniforms(a->seed, (uint32_t)(depth + 32 * i), a->round, rid, &u, NULL);
+            if (acc < 1.0) {
+                double mm = fabs(u - acc);
+                if (mm < mu) mu = mm;
+                if (u >= acc) continue;                     /* reject: next candidate */
+            }
+            next = c;
+            break;
+        }
+        if (status & SD_REF_HARD_FAULTS) break;
+        if (next >= 0) {
+            tokens[depth] = a->tok[(size_t)b * a->N + next];
+            n = next;
+            ++depth;
+            continue;
+        }
+        /* every candidate rejected: t ~ d_m */
+        if (residual_step(pb, qb, V) == 0.0) status |= SD_REF_FAULT_ZERO_RESIDUAL;
+        double R = 0.0;
+        for (int32_t y = 0; y < V; ++y) R += pb[y];
+        double us, Cp, Ct;
+        sd_ref_uniforms(a->seed, (uint32_t)depth, a->round, rid, NULL, &us);
+        double th = us * R;
+        tokens[depth] = inverse_cdf(pb, V, th, &Cp, &Ct);
+        double m1 = th - Cp, m2 = Ct - th, ms = (m1 < m2 ? m1 : m2) / R;
+        if (ms < mu) mu = ms;
+        break;
+    }
+    (void)outc;
+    if (status & SD_REF_HARD_FAULTS) {
+        for (int32_t i = 0; i <= d; ++i) tokens[i] = -1;
+        depth = 0;
+    }
+    *out_L = depth;
+    if (node_out) *node_out = n;
+    if (mu_out) *mu_out = mu;
+    return status;
+}
+
+int sd_ref_tree_verify(const void* p, const void* q, const int32_t* tok, int32_t B, int32_t m,
+                       int32_t d, int32_t V, int64_t ld_p, int64_t ld_q, int32_t dtype, double T,
+                       uint64_t seed, uint64_t round, uint64_t rid_base, int32_t* out_L,
+                       int32_t* out_tokens, int32_t* out_status, int32_t* out_node,
+                       double* out_mu) {
+    if (!p || !tok || !out_L || !out_tokens || B < 0 || m < 1 || m > 8 || d < 1 || d > SD_REF_KMAX ||
+        V < 2 || (dtype != 0 && dtype != 1) || !(T >= 0.0) || isinf(T) || (T > 0.0 && !q))
+        return 1;
+    if (ld_p == 0) ld_p = V;
+    if (ld_q == 0) ld_q = V;
+    int64_t N = 0, Nint = 0, w = 1;
+    for (int32_t t = 0; t <= d; ++t) { N += w; if (t < d) Nint += w; w *= m; if (N > (1 << 24)) return 1; }
+    tree_t a = {p, q, tok, m, d, V, (int32_t)N, (int32_t)Nint, ld_p, ld_q, dtype, T, seed, round, rid_base};
+    double* pb = (double*)malloc(sizeof(double) * (size_t)V);
+    double* qb = (double*)malloc(sizeof(double) * (size_t)V);
+    for (int32_t b = 0; b < B; ++b) {
+        int st = tree_one(&a, b, &out_L[b], out_tokens + (size_t)b * (d + 1),
+                          out_node ? &out_node[b] : NULL, out_mu ? &out_mu[b] : NULL, pb, qb, NULL);
+        if (out_status) out_status[b] = st;
+    }
+    free(pb);
+    free(qb);
+    return 0;
+}
+
+/* Exact outcome distribution of one tree verify with the uniforms integrated out:
+ * out[b][n][y] = Pr(the walk stops at node n and emits token y), fixed tree (T > 0). */
+int sd_ref_tree_outcome_dist(const void* p, const void* q, const int32_t* tok, int32_t B,
+                             int32_t m, int32_t d, int32_t V, int64_t ld_p, int64_t ld_q,
+                             int32_t dtype, double T, double* out) {
+    if (!p || !q || !tok || !out || m < 1 || d < 1 || V < 2 || !(T > 0.0)) return 1;
+    if (ld_p == 0) ld_p = V;
+    if (ld_q == 0) ld_q = V;
+    int64_t N = 0, Nint = 0, w = 1;
+    for (int32_t t = 0; t <= d; ++t) { N += w; if (t < d) Nint += w; w *= m; if (N > (1 << 20)) return 1; }
+    tree_t a = {p, q, tok, m, d, V, (int32_t)N, (int32_t)Nint, ld_p, ld_q, dtype, T, 0, 0, 0};
+    memset(out, 0, sizeof(double) * (size_t)B * N * V);
+    double* pb = (double*)malloc(sizeof(double) * (size_t)V);
+    double* qb = (double*)malloc(sizeof(double) * (size_t)V);
+    double* reach = (double*)malloc(sizeof(double) * (size_t)N);
+    int32_t* depth_of = (int32_t*)malloc(sizeof(int32_t) * (size_t)N);
+    for (int32_t b = 0; b < B; ++b) {
+        double* ob = out + (size_t)b * N * V;
+        for (int64_t n = 0; n < N; ++n) reach[n] = 0.0;
+        reach[0] = 1.0;
+        depth_of[0] = 0;
+        for (int64_t n = 0; n < N; ++n) {                   /* level order: parents first */
+            if (n > 0) depth_of[n] = depth_of[(n - 1) / m] + 1;
+            if (reach[n] == 0.0) continue;
+            row_t pr = tree_p(&a, b, (int32_t)n);
+            double lp = row_logsumexp(pr, T);
+            for (int32_t y = 0; y < V; ++y) pb[y] = prob_of(pr, y, T, lp);
+            if (depth_of[n] == d) {                         /* leaf: bonus */
+                for (int32_t y = 0; y < V; ++y) ob[(size_t)n * V + y] += reach[n] * pb[y];
+                continue;
+            }
+            row_t qr = tree_q(&a, b, (int32_t)n);
+            double lq = row_logsumexp(qr, T);
+            for (int32_t y = 0; y < V; ++y) qb[y] = prob_of(qr, y, T, lq);
+            double stay = reach[n];                         /* Pr(at n, all earlier candidates rejected) */
+            for (int32_t i = 0; i < m; ++i) {
+                int32_t c = (int32_t)(m * n + 1 + i), x = tok[(size_t)b * N + c];
+                if (i > 0) residual_step(pb, qb, V);
+                double acc = qb[x] > 0.0 ? (pb[x] >= qb[x] ? 1.0 : pb[x] / qb[x]) : 0.0;
+                reach[c] += stay * acc;
+                stay *= 1.0 - acc;
+            }
+            residual_step(pb, qb, V);
+            for (int32_t y = 0; y < V; ++y) ob[(size_t)n * V + y] += stay * pb[y];
+        }
+    }
+    free(pb); free(qb); free(reach); free(depth_of);
+    return 0;
+}

@@ -99,6 +99,18 @@ int sd_ref_draft_sample(const void* q, int32_t B, int32_t k, int32_t V, int64_t 
                         int32_t dtype, double T, uint64_t seed, uint64_t round, uint64_t rid_base,
                         int32_t* out_ids, double* out_logq, double* out_mu, int32_t* out_status);
 
+/* Lossless tree verification (NEXT-3, reading D-2): recursive rejection sampling over the m
+ * i.i.d. children of each node of a full m-ary depth-d tree (level order).  See the .c file. */
+int sd_ref_tree_verify(const void* p, const void* q, const int32_t* tok, int32_t B, int32_t m,
+                       int32_t d, int32_t V, int64_t ld_p, int64_t ld_q, int32_t dtype, double T,
+                       uint64_t seed, uint64_t round, uint64_t rid_base, int32_t* out_L,
+                       int32_t* out_tokens, int32_t* out_status, int32_t* out_node,
+                       double* out_mu);
+/* Exact Pr(stop at node n, emit y) of one tree verify, uniforms integrated out (T > 0). */
+int sd_ref_tree_outcome_dist(const void* p, const void* q, const int32_t* tok, int32_t B,
+                             int32_t m, int32_t d, int32_t V, int64_t ld_p, int64_t ld_q,
+                             int32_t dtype, double T, double* out);
+
 /* Eq. (1): beta = sum_x min{p(x), q(x)} for p = softmax(zp/T), q = softmax(zq/T) (fp32 logits). */
 double sd_ref_beta(const float* zp, const float* zq, int32_t V, double T);
 /* softmax at temperature T of one fp32 logit row, fp64 out. */

@@ -21,10 +21,16 @@ MUTATIONS = [
     ("sampling_dist: no C-6 fallback", "        if (R > 0.0) return R;\n        *zero_res = 1;", "        return R;\n        *zero_res = 1;"),
     ("sampling_dist: residual q - p", "double d = prob_of(pr, y, T, lam_p) - prob_of(*qr, y, T, lam_q);",
      "double d = prob_of(*qr, y, T, lam_q) - prob_of(pr, y, T, lam_p);"),
+    ("tree: no residual between candidates (outcome)", "                if (i > 0) residual_step(pb, qb, V);\n                double acc = qb[x] > 0.0",
+     "                double acc = qb[x] > 0.0"),
+    ("tree: final sample from p, not d_m (walk)", "        /* every candidate rejected: t ~ d_m */\n        if (residual_step(pb, qb, V) == 0.0) status |= SD_REF_FAULT_ZERO_RESIDUAL;",
+     "        /* every candidate rejected: t ~ d_m */"),
+    ("tree: candidate counter without the 32 i stride", "sd_ref_uniforms(a->seed, (uint32_t)(depth + 32 * i), a->round, rid, &u, NULL);",
+     "sd_ref_uniforms(a->seed, (uint32_t)(depth + i), a->round, rid, &u, NULL);"),
     ("verify: u_acc from w1", "sd_ref_uniforms(a->seed, (uint32_t)j, a->round, rid, &u_acc, NULL);",
      "sd_ref_uniforms(a->seed, (uint32_t)j, a->round, rid, NULL, &u_acc);"),
 ]
-SUITES = ["tests/test_oracle_checkers.py", "tests/test_oracle_pins.py"]
+SUITES = ["tests/test_oracle_checkers.py", "tests/test_oracle_pins.py", "tests/test_oracle_tree.py"]
 
 
 def main():
