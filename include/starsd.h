@@ -255,6 +255,36 @@ sd_status sd_verify_qmeta(const void* p_logits, const void* q_logits, const sd_q
                           void* workspace, size_t workspace_bytes, cudaStream_t stream);
 
 /*
+ * sd_tree_verify -- lossless verification of a draft TREE.  The paper drafts
+ * a depth-d tree with branching k (Alg. 2) and keeps the best of its
+ * independently verified paths, which is not lossless; this call instead
+ * walks the tree by recursive rejection sampling over the children of each node (reading D-2,
+ * SpecInfer's multi-candidate rule, ref. [miao2024specinfer] at P:80): the `branching` children of
+ * a node are i.i.d. draws from the node's draft distribution q; with d_0 = p,
+ *   accept child i iff u_i < min(1, d_{i-1}(x_i) / q(x_i)) -> descend;
+ *   else d_i = norm(max(0, d_{i-1} - q)) (the residual of P:736, applied again);
+ *   all children rejected: emit t ~ d_m;  a leaf (depth d) reached: the bonus t ~ p_leaf.
+ * branching = 1 is exactly sd_verify's chain (same Philox counters).  T = 0: descend into the first
+ * child whose token is argmax p_node, else emit argmax p_node.
+ * Layout: full m-ary trees (m = branching), level order: node 0 = root, children of n are
+ * m n + 1 .. m n + m; N = sum_{t <= d} m^t nodes, N_int = sum_{t < d} m^t internal nodes.
+ *   p_logits    device [B][N][ld_p]: target logits at every node (after the node's prefix)
+ *   q_logits    device [B][N_int][ld_q]: draft logits at internal nodes (NULL iff T == 0)
+ *   tree_tokens device [B][N] int32: each node's token (the root's entry is unused)
+ *   shape       batch = B, k = depth d (1..31), vocab, ld_p, ld_q, dtype
+ *   uniforms    child i at depth t: u24(w0) of counter (t + 32 i, round, rid); the emitted token
+ *               at depth t: u24(w1) of (t, round, rid); rid = request_id_base + b (C-8)
+ *   out_accept_len [B] = depth reached; out_tokens [B][d+1] = the accepted path's tokens, the
+ *   emitted token, then -1; out_status [B] (nullable) fault bits; out_node [B] (nullable) = the
+ *   node the walk stopped at.  One CTA per request; no workspace.
+ */
+sd_status sd_tree_verify(const void* p_logits, const void* q_logits, const int32_t* tree_tokens,
+                         const sd_shape* shape, int32_t branching, float temperature,
+                         uint64_t seed, uint64_t round, uint64_t request_id_base,
+                         int32_t* out_accept_len, int32_t* out_tokens, int32_t* out_status,
+                         int32_t* out_node, cudaStream_t stream);
+
+/*
  * sd_debug_trace -- development instrumentation (library built with STARSD_BUILD_DEBUG=1;
  * otherwise ignored).  When device_buf != NULL, subsequent sd_verify calls on this thread write
  * eight uint64 per k_row_stats CTA: %globaltimer at phase points 0..6 and word 7 = smid << 32 |

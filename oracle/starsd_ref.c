@@ -663,8 +663,14 @@ static int tree_one(const tree_t* a, int32_t b, int32_t* out_L, int32_t* tokens,
             if (x < 0 || x >= V) { status = SD_REF_FAULT_BAD_DRAFT_ID; break; }
             if (i > 0 && residual_step(pb, qb, V) == 0.0) status |= SD_REF_FAULT_ZERO_RESIDUAL;
             double u, acc;
-            if (!(qb[x] > 0.0)) { acc = 0.0; }               /* C-7: q(x) = 0 rejects */
-            else acc = pb[x] >= qb[x] ? 1.0 : pb[x] / qb[x];
+            if (z_of(qr, x) == -INFINITY) {                  /* C-7: q(x) = 0 rejects */
+                acc = 0.0;
+                status |= SD_REF_FAULT_ZERO_Q;
+            } else if (!(qb[x] > 0.0)) {
+                acc = pb[x] > 0.0 ? 1.0 : 0.0;               /* (underflowed q: the limit) */
+            } else {
+                acc = pb[x] >= qb[x] ? 1.0 : pb[x] / qb[x];
+            }
             sd_ref_uniforms(a->seed, (uint32_t)(depth + 32 * i), a->round, rid, &u, NULL);
             if (acc < 1.0) {
                 double mm = fabs(u - acc);

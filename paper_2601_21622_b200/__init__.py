@@ -13,7 +13,7 @@ import torch
 from . import _lib
 from ._lib import StarsdError, check
 
-__all__ = ["verify", "verify_qmeta", "verify_host", "verify_trace", "draft_sample", "draft_qmeta",
+__all__ = ["verify", "verify_qmeta", "tree_verify", "verify_host", "verify_trace", "draft_sample", "draft_qmeta",
            "qmeta_fields", "workspace_size", "draft_workspace_size", "plan", "philox_words",
            "Workspace", "StarsdError", "version"]
 
@@ -266,6 +266,40 @@ def verify_qmeta(p: torch.Tensor, q: torch.Tensor, qmeta: torch.Tensor, ids: tor
                                       ws.buf.data_ptr(), ws.nbytes, s.cuda_stream),
           "sd_verify_qmeta")
     return L, tok, st
+
+
+def tree_verify(p: torch.Tensor, q: torch.Tensor | None, tree_tokens: torch.Tensor, branching: int,
+                temperature: float, seed: int = 0, round: int = 0, request_id_base: int = 0,
+                vocab: int | None = None, stream: torch.cuda.Stream | None = None):
+    """sd_tree_verify (NEXT-3): p [B, N, ld], q [B, N_int, ld] (None at T = 0), tree_tokens
+    [B, N] int32 for full `branching`-ary trees of depth d in level order.  Returns (accept_len
+    [B], tokens [B, d+1], status [B], stop node [B])."""
+    B, N, ld_p = p.shape
+    m = branching
+    d, n, w = 0, 1, 1
+    while n < N:
+        w *= m
+        n += w
+        d += 1
+    if n != N or d < 1:
+        raise StarsdError(f"p holds {N} nodes: not a full {m}-ary tree")
+    if tree_tokens.shape != (B, N) or tree_tokens.dtype != torch.int32 or not tree_tokens.is_contiguous():
+        raise StarsdError("tree_tokens must be a contiguous int32 [B, N] tensor")
+    code = _dtype_code(p)
+    ld_q = q.shape[-1] if q is not None else ld_p
+    V = ld_p if vocab is None else vocab
+    L = torch.empty(B, dtype=torch.int32, device=p.device)
+    tok = torch.empty(B, d + 1, dtype=torch.int32, device=p.device)
+    st = torch.empty(B, dtype=torch.int32, device=p.device)
+    node = torch.empty(B, dtype=torch.int32, device=p.device)
+    s = stream if stream is not None else torch.cuda.current_stream(p.device)
+    sh = _shape(B, d, V, ld_p, ld_q, code)
+    check(_lib.load().sd_tree_verify(p.data_ptr(), q.data_ptr() if q is not None else None,
+                                     tree_tokens.data_ptr(), ctypes.byref(sh), m, float(temperature),
+                                     seed & (2**64 - 1), round & (2**64 - 1),
+                                     request_id_base & (2**64 - 1), L.data_ptr(), tok.data_ptr(),
+                                     st.data_ptr(), node.data_ptr(), s.cuda_stream), "sd_tree_verify")
+    return L, tok, st, node
 
 
 def verify_host(p: torch.Tensor, q: torch.Tensor | None, ids: torch.Tensor, temperature: float,

@@ -26,7 +26,8 @@ EXPORTS = ["sd_verify", "sd_verify_workspace_size", "sd_philox_uniforms", "sd_st
            "sd_star_analytics", "sd_star_observe", "sd_star_predict", "sd_star_draft_begin_v",
            "sd_sched_create", "sd_sched_push", "sd_sched_pop", "sd_sched_service",
            "sd_sched_observe", "sd_sched_stats", "sd_sched_predict", "sd_sched_destroy",
-           "sd_draft_workspace_size", "sd_draft_sample", "sd_draft_qmeta", "sd_verify_qmeta"]
+           "sd_draft_workspace_size", "sd_draft_sample", "sd_draft_qmeta", "sd_verify_qmeta",
+           "sd_tree_verify"]
 
 
 class Shape(ctypes.Structure):
@@ -114,6 +115,9 @@ def load():
     L.sd_draft_sample.restype = st
     L.sd_draft_qmeta.argtypes = [vp, vp, ctypes.POINTER(Shape), ctypes.c_float, vp, vp, sz, vp]
     L.sd_draft_qmeta.restype = st
+    L.sd_tree_verify.argtypes = [vp, vp, vp, ctypes.POINTER(Shape), i32, ctypes.c_float, u64, u64,
+                                 u64, vp, vp, vp, vp, vp]
+    L.sd_tree_verify.restype = st
     L.sd_verify_trace.argtypes = [ctypes.POINTER(Shape), ctypes.c_float, vp, vp, vp, vp, vp, vp, vp]
     L.sd_verify_trace.restype = st
     L.sd_philox_uniforms.argtypes = [u64, u64, vp, vp, i32, vp, vp]

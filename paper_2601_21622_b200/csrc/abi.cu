@@ -24,6 +24,20 @@ cudaError_t launch_trace(const Params& P, const int32_t* accept_len, double* lam
                          double* a, double* R, cudaStream_t st);
 cudaError_t launch_qmeta(const Params& P, bool bf16, const int32_t* ids, QMeta* out,
                          cudaStream_t st);
+struct TreeParams {
+    const void* p;
+    const void* q;
+    const int32_t* tok;
+    int32_t B, m, d, V, N, Nint;
+    int64_t ld_p, ld_q;
+    float c2;
+    uint64_t seed, round, rid_base;
+    int32_t* out_L;
+    int32_t* out_tok;
+    int32_t* out_status;
+    int32_t* out_node;
+};
+cudaError_t launch_tree(const TreeParams& P, bool bf16, cudaStream_t st);
 cudaError_t qmeta_gather(const Params& P, bool bf16, const int32_t* ids, QMeta* out,
                          cudaStream_t st);
 
@@ -142,6 +156,7 @@ static void fill_params(Params& P, const sd_shape* shape, int esz, float tempera
     P.ticketA = reinterpret_cast<uint32_t*>(ws + w.ticketA);
     P.ticketB = reinterpret_cast<uint32_t*>(ws + w.ticketB);
     P.tailT = reinterpret_cast<uint32_t*>(ws + w.tailT);
+    P.work = reinterpret_cast<uint32_t*>(ws + w.work);
     P.rowstat = reinterpret_cast<RowStat*>(ws + w.rowstat);
     P.partA = reinterpret_cast<PartA*>(ws + w.partA);
     P.partB = reinterpret_cast<PartB*>(ws + w.partB);
@@ -153,6 +168,8 @@ static void fill_params(Params& P, const sd_shape* shape, int esz, float tempera
     static const int chain = env_flag("STARSD_CHAIN", 1);   // 0: plain stream order
     P.chain = chain ? 1 : 0;
     P.esz = esz;
+    static const int persist = env_flag("STARSD_PERSIST", 0);   // A/B knob
+    P.persist = persist ? 1 : 0;
 }
 
 }  // namespace sd
@@ -341,6 +358,55 @@ sd_status sd_draft_qmeta(const void* q_logits, const int32_t* draft_ids, const s
     if (temperature == 0.0f) return fail(SD_ERR_INVALID_ARGUMENT, "sd_draft_qmeta: T > 0 only");
     return draft_call(q_logits, draft_ids, shape, temperature, 0, 0, 0, nullptr, out_qmeta,
                       nullptr, workspace, workspace_bytes, stream);
+}
+
+sd_status sd_tree_verify(const void* p_logits, const void* q_logits, const int32_t* tree_tokens,
+                         const sd_shape* shape, int32_t branching, float temperature,
+                         uint64_t seed, uint64_t round, uint64_t request_id_base,
+                         int32_t* out_accept_len, int32_t* out_tokens, int32_t* out_status,
+                         int32_t* out_node, cudaStream_t stream) {
+    clear_error();
+    int esz;
+    sd_status s = check_shape(shape, temperature, &esz);
+    if (s != SD_OK) return s;
+    if (branching < 1 || branching > 8)
+        return fail(SD_ERR_INVALID_ARGUMENT, "branching=%d outside [1, 8]", branching);
+    int64_t N = 0, Nint = 0, w = 1;
+    for (int t = 0; t <= shape->k; ++t) {
+        N += w;
+        if (t < shape->k) Nint += w;
+        w *= branching;
+        if (N > (1 << 20)) return fail(SD_ERR_UNSUPPORTED, "tree of more than 2^20 nodes");
+    }
+    if (shape->batch == 0) return SD_OK;
+    const bool greedy = temperature == 0.0f;
+    if (!p_logits || (!greedy && !q_logits) || !tree_tokens || !out_accept_len || !out_tokens)
+        return fail(SD_ERR_INVALID_ARGUMENT, "NULL pointer");
+    if (!aligned16(p_logits) || (!greedy && !aligned16(q_logits)))
+        return fail(SD_ERR_INVALID_ARGUMENT, "p_logits / q_logits not 16-byte aligned");
+    TreeParams P{};
+    P.p = p_logits;
+    P.q = greedy ? nullptr : q_logits;
+    P.tok = tree_tokens;
+    P.B = shape->batch;
+    P.m = branching;
+    P.d = shape->k;
+    P.V = shape->vocab;
+    P.N = static_cast<int32_t>(N);
+    P.Nint = static_cast<int32_t>(Nint);
+    P.ld_p = shape->ld_p ? shape->ld_p : shape->vocab;
+    P.ld_q = shape->ld_q ? shape->ld_q : shape->vocab;
+    P.c2 = greedy ? 0.0f : static_cast<float>(1.4426950408889634 / static_cast<double>(temperature));
+    P.seed = seed;
+    P.round = round;
+    P.rid_base = request_id_base;
+    P.out_L = out_accept_len;
+    P.out_tok = out_tokens;
+    P.out_status = out_status;
+    P.out_node = out_node;
+    cudaError_t e = launch_tree(P, shape->dtype == SD_DTYPE_BF16, stream);
+    if (e != cudaSuccess) return fail(SD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return SD_OK;
 }
 
 sd_status sd_verify_trace(const sd_shape* shape, float temperature, const void* workspace,

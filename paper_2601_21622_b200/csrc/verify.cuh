@@ -83,6 +83,7 @@ struct Params {
     uint32_t* ticketA;           // [B][k+1] row tickets (tagged rows: start order; else arrival)
     uint32_t* ticketB;           // [B]    sampling chunk tasks finished
     uint32_t* tailT;             // [B]    k_sample_chunked CTAs finished
+    uint32_t* work;              // [1]    persistent k_row_stats: next work item to claim
     RowStat* rowstat;            // [B][k+1]
     PartA* partA;                // [B][k+1][nch]
     PartB* partB;                // [B][nch]
@@ -102,6 +103,8 @@ struct Params {
     int32_t chain;               // k_row_stats launched as a programmatic dependent of whatever
                                  // kernel precedes it on the stream (griddepcontrol.wait first)
     int32_t esz;                 // bytes per logit
+    int32_t persist;             // tagged rows run as k_row_stats_persist (resident CTAs claiming
+                                 // work items) instead of one CTA per item
     const QMeta* qmeta;          // [B][k] draft-row metadata: the q rows are then read only at the
                                  // stop position (sd_verify_qmeta); NULL: full q rows
 };
@@ -132,7 +135,7 @@ inline int32_t row_cluster(int32_t nch) {
 // Workspace layout for a shape; all offsets 16-byte aligned.  The first `zero_bytes` must be
 // zero before a call and are zero again after it (word 0, the call counter, excepted).
 struct WsLayout {
-    size_t epoch, state, ticketA, ticketB, tailT, zero_bytes;
+    size_t epoch, state, ticketA, ticketB, tailT, work, zero_bytes;
     size_t rowstat, partA, partB, segtab, rres, partT, total;
 };
 
@@ -159,6 +162,7 @@ inline WsLayout ws_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
     w.ticketA = o;  o = align16(o + sizeof(uint32_t) * (size_t)B * (k + 1));
     w.ticketB = o;  o = align16(o + sizeof(uint32_t) * B);
     w.tailT = o;    o = align16(o + sizeof(uint32_t) * B);
+    w.work = o;     o = align16(o + sizeof(uint32_t));
     w.zero_bytes = o;
     w.rowstat = o;  o = align16(o + sizeof(RowStat) * (size_t)B * (k + 1));
     w.partA = o;    o = align16(o + sizeof(PartA) * (size_t)B * (k + 1) * nch);

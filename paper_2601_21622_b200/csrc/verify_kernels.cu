@@ -890,6 +890,146 @@ __device__ __forceinline__ void sample_task(const Params& P, unsigned char* smem
     }
 }
 
+// The slice partial of one chunk (whole CTA; valid in warp 0, zx fields in lane 0): wait for the
+// bulk copies (mbarrier parities ph0 / ph1), unpack NV vectors per thread into registers, the lean
+// statistics (or argmax) per thread, warp and block reductions.
+template <typename E, bool GREEDY>
+__device__ __forceinline__ PartA slice_partial(const Params& P, const E* sp, const E* sq, int c0,
+                                               int len, bool load_q, int x, uint64_t* bar,
+                                               uint32_t ph0, uint32_t ph1, float (*s_d)[kWarps],
+                                               double (*s_s)[kWarps], int* s_gi, int* s_f) {
+    using EL = Elt<E>;
+    constexpr int VEC = EL::VEC;
+    constexpr int NV = kMaxChunkBytes / kVecBytes / kThreads;   // 16-byte vectors per thread
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // ---- registers: NV vectors of p (and q) per thread; -inf past the slice end ------------
+    const int nfull = len / VEC;                 // complete vectors
+    const int nvv = (len + VEC - 1) / VEC;       // vectors incl. a ragged last one
+    float vp[NV][VEC];
+    mbar_wait(&bar[0], ph0);   // (the copy is in flight: it completes)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int g = tid + i * kThreads;
+        if (g < nfull) {
+            EL::unpack(*reinterpret_cast<const uint4*>(sp + g * VEC), vp[i]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) vp[i][e] = -INFINITY;
+            if (g < nvv) {   // ragged last vector (row end only)
+#pragma unroll
+                for (int e = 0; e < VEC; ++e)
+                    if (g * VEC + e < len) vp[i][e] = EL::one(sp, g * VEC + e);
+            }
+        }
+    }
+    int nf = 0;
+    float dP = -INFINITY, dQ = -INFINITY, sP = 0.0f, sQ = 0.0f;
+    float gbest = -INFINITY;
+    int gidx = INT_MAX;
+    if (GREEDY) {
+        float nanacc = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            float vm = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < VEC; e += 2) {
+                nanacc = max3nan(nanacc, vp[i][e], vp[i][e + 1]);
+                vm = max3(vm, vp[i][e], vp[i][e + 1]);
+            }
+            if (vm > gbest) {   // ascending index within the thread: strict > keeps the first
+                int fe = 0;
+#pragma unroll
+                for (int e = VEC - 1; e >= 0; --e)
+                    if (vp[i][e] == vm) fe = e;
+                gbest = vm;
+                gidx = c0 + (tid + i * kThreads) * VEC + fe;
+            }
+        }
+        if (!(nanacc < INFINITY)) nf |= kPartNonfiniteP;
+    } else {
+        thread_stats<NV, VEC>(vp, P.c2, kPartNonfiniteP, dP, sP, nf);
+        if (load_q) {
+            float vq[NV][VEC];
+            mbar_wait(&bar[1], ph1);
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int g = tid + i * kThreads;
+                if (g < nfull) {
+                    EL::unpack(*reinterpret_cast<const uint4*>(sq + g * VEC), vq[i]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) vq[i][e] = -INFINITY;
+                    if (g < nvv) {
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e)
+                            if (g * VEC + e < len) vq[i][e] = EL::one(sq, g * VEC + e);
+                    }
+                }
+            }
+            thread_stats<NV, VEC>(vq, P.c2, kPartNonfiniteQ, dQ, sQ, nf);
+        }
+    }
+
+    // ---- block reduction: warps, then warp 0 ---------------------------------------------
+    nf = __reduce_or_sync(0xFFFFFFFFu, nf);
+    if (GREEDY) {
+        float v = gbest;
+        int i = gidx;
+        warp_argmax(v, i);
+        if (lane == 0) {
+            s_d[0][warp] = v;
+            s_gi[warp] = i;
+            s_f[warp] = nf;
+        }
+    } else {
+        const float Dw = warp_max(dP), Ew = warp_max(dQ);
+        const double Sw = warp_sum(sP > 0.0f ? static_cast<double>(sP * ex2_approx(dP - Dw)) : 0.0);
+        const double Tw = warp_sum(sQ > 0.0f ? static_cast<double>(sQ * ex2_approx(dQ - Ew)) : 0.0);
+        if (lane == 0) {
+            s_d[0][warp] = Dw;
+            s_d[1][warp] = Ew;
+            s_s[0][warp] = Sw;
+            s_s[1][warp] = Tw;
+            s_f[warp] = nf;
+        }
+    }
+    __syncthreads();
+    PartA pa{};
+    if (warp == 0) {
+        const bool on = lane < kWarps;
+        const int f = __reduce_or_sync(0xFFFFFFFFu, on ? s_f[lane] : 0);
+        if (GREEDY) {
+            float v = on ? s_d[0][lane] : -INFINITY;
+            int i = on ? s_gi[lane] : INT_MAX;
+            warp_argmax(v, i);
+            pa.M_p = v;
+            pa.M_q = -INFINITY;
+            pa.S_p = pa.S_q = 0.0;
+            pa.argmax = i;
+        } else {
+            const float wd = on ? s_d[0][lane] : -INFINITY, we = on ? s_d[1][lane] : -INFINITY;
+            const double ws = on ? s_s[0][lane] : 0.0, wt = on ? s_s[1][lane] : 0.0;
+            const float Dc = warp_max(wd), Ec = warp_max(we);
+            pa.S_p = warp_sum(ws > 0.0 ? ws * static_cast<double>(ex2_approx(wd - Dc)) : 0.0);
+            pa.S_q = warp_sum(wt > 0.0 ? wt * static_cast<double>(ex2_approx(we - Ec)) : 0.0);
+            pa.M_p = Dc;   // scaled maxima D (see resid_terms)
+            pa.M_q = Ec;
+            pa.argmax = INT_MAX;
+        }
+        if (lane == 0) {
+            pa.zx_p = 0.0f;
+            pa.zx_q = 0.0f;
+            pa.flags = f;
+            if (x >= c0 && x < c0 + len) {
+                pa.zx_p = EL::one(sp, x - c0);
+                pa.zx_q = load_q ? EL::one(sq, x - c0) : 0.0f;
+                pa.flags |= kPartHasX;
+            }
+        }
+    }
+    return pa;
+}
+
 // ------------------------------------------------------------------------------------------
 // Kernel A: per-slice statistics + per-row acceptance decision (+ sampling chunk tasks)
 //
@@ -1014,134 +1154,12 @@ __global__ void __launch_bounds__(kThreads, GREEDY ? 8 : 6) k_row_stats(const Pa
     if (CL > 1) cl_wait_acquire();   // (copies in flight) the leader's s_pbar is initialised
     __syncthreads();
 
-    // ---- registers: NV vectors of p (and q) per thread; -inf past the slice end ------------
-    const int nfull = len / VEC;                 // complete vectors
-    const int nvv = (len + VEC - 1) / VEC;       // vectors incl. a ragged last one
-    float vp[NV][VEC];
-    mbar_wait(&bar[0], 0);   // (the copy is in flight: it completes)
-    if (tid == 0) SD_TR(P, 2);
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int g = tid + i * kThreads;
-        if (g < nfull) {
-            EL::unpack(*reinterpret_cast<const uint4*>(sp + g * VEC), vp[i]);
-        } else {
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) vp[i][e] = -INFINITY;
-            if (g < nvv) {   // ragged last vector (row end only)
-#pragma unroll
-                for (int e = 0; e < VEC; ++e)
-                    if (g * VEC + e < len) vp[i][e] = EL::one(sp, g * VEC + e);
-            }
-        }
-    }
-    int nf = 0;
-    float dP = -INFINITY, dQ = -INFINITY, sP = 0.0f, sQ = 0.0f;
-    float gbest = -INFINITY;
-    int gidx = INT_MAX;
-    if (GREEDY) {
-        float nanacc = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            float vm = -INFINITY;
-#pragma unroll
-            for (int e = 0; e < VEC; e += 2) {
-                nanacc = max3nan(nanacc, vp[i][e], vp[i][e + 1]);
-                vm = max3(vm, vp[i][e], vp[i][e + 1]);
-            }
-            if (vm > gbest) {   // ascending index within the thread: strict > keeps the first
-                int fe = 0;
-#pragma unroll
-                for (int e = VEC - 1; e >= 0; --e)
-                    if (vp[i][e] == vm) fe = e;
-                gbest = vm;
-                gidx = c0 + (tid + i * kThreads) * VEC + fe;
-            }
-        }
-        if (!(nanacc < INFINITY)) nf |= kPartNonfiniteP;
-    } else {
-        thread_stats<NV, VEC>(vp, P.c2, kPartNonfiniteP, dP, sP, nf);
-        if (load_q) {
-            float vq[NV][VEC];
-            mbar_wait(&bar[1], 0);
-            if (tid == 0) SD_TR(P, 3);
-#pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                const int g = tid + i * kThreads;
-                if (g < nfull) {
-                    EL::unpack(*reinterpret_cast<const uint4*>(sq + g * VEC), vq[i]);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < VEC; ++e) vq[i][e] = -INFINITY;
-                    if (g < nvv) {
-#pragma unroll
-                        for (int e = 0; e < VEC; ++e)
-                            if (g * VEC + e < len) vq[i][e] = EL::one(sq, g * VEC + e);
-                    }
-                }
-            }
-            thread_stats<NV, VEC>(vq, P.c2, kPartNonfiniteQ, dQ, sQ, nf);
-        }
-    }
-
-    // ---- block reduction: warps, then warp 0 ---------------------------------------------
-    nf = __reduce_or_sync(0xFFFFFFFFu, nf);
-    if (GREEDY) {
-        float v = gbest;
-        int i = gidx;
-        warp_argmax(v, i);
-        if (lane == 0) {
-            s_d[0][warp] = v;
-            s_gi[warp] = i;
-            s_f[warp] = nf;
-        }
-    } else {
-        const float Dw = warp_max(dP), Ew = warp_max(dQ);
-        const double Sw = warp_sum(sP > 0.0f ? static_cast<double>(sP * ex2_approx(dP - Dw)) : 0.0);
-        const double Tw = warp_sum(sQ > 0.0f ? static_cast<double>(sQ * ex2_approx(dQ - Ew)) : 0.0);
-        if (lane == 0) {
-            s_d[0][warp] = Dw;
-            s_d[1][warp] = Ew;
-            s_s[0][warp] = Sw;
-            s_s[1][warp] = Tw;
-            s_f[warp] = nf;
-        }
-    }
-    __syncthreads();
+    const PartA pa0 = slice_partial<E, GREEDY>(P, sp, sq, c0, len, load_q, x, bar, 0u, 0u, s_d, s_s,
+                                                s_gi, s_f);
     if (tid == 0) SD_TR(P, 4);
     if ((CL > 1 || TAG) && warp != 0) return;
     if (warp == 0) {
-        const bool on = lane < kWarps;
-        const int f = __reduce_or_sync(0xFFFFFFFFu, on ? s_f[lane] : 0);
-        PartA pa;
-        if (GREEDY) {
-            float v = on ? s_d[0][lane] : -INFINITY;
-            int i = on ? s_gi[lane] : INT_MAX;
-            warp_argmax(v, i);
-            pa.M_p = v;
-            pa.M_q = -INFINITY;
-            pa.S_p = pa.S_q = 0.0;
-            pa.argmax = i;
-        } else {
-            const float wd = on ? s_d[0][lane] : -INFINITY, we = on ? s_d[1][lane] : -INFINITY;
-            const double ws = on ? s_s[0][lane] : 0.0, wt = on ? s_s[1][lane] : 0.0;
-            const float Dc = warp_max(wd), Ec = warp_max(we);
-            pa.S_p = warp_sum(ws > 0.0 ? ws * static_cast<double>(ex2_approx(wd - Dc)) : 0.0);
-            pa.S_q = warp_sum(wt > 0.0 ? wt * static_cast<double>(ex2_approx(we - Ec)) : 0.0);
-            pa.M_p = Dc;   // scaled maxima D (see resid_terms)
-            pa.M_q = Ec;
-            pa.argmax = INT_MAX;
-        }
-        if (lane == 0) {
-            pa.zx_p = 0.0f;
-            pa.zx_q = 0.0f;
-            pa.flags = f;
-            if (x >= c0 && x < c0 + len) {
-                pa.zx_p = EL::one(sp, x - c0);
-                pa.zx_q = load_q ? EL::one(sq, x - c0) : 0.0f;
-                pa.flags |= kPartHasX;
-            }
-        }
+        PartA pa = pa0;
         if (CL > 1) {
             cluster_publish<GREEDY, CL>(P, pa, s_parts, &s_pbar, rank, c / CL, b, j, x, lane);
             return;
@@ -1194,6 +1212,125 @@ __global__ void __launch_bounds__(kThreads, GREEDY ? 8 : 6) k_row_stats(const Pa
     if (tid == 0) { SD_TR(P, 6); SD_TRF(P, 2); }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Kernel A, persistent form (rows of 2..64 chunks, STARSD_PERSIST): the same work items as
+// k_row_stats' grid -- (chunk c, request b, position j), position-major -- but claimed one at a time
+// from a global counter by CTAs that stay resident (occupancy x SMs of them).  A skipped item
+// (its request stopped below j) costs a branch, not a CTA launch; the claim of the next item and
+// its request's state word are prefetched while the current item streams and reduces, so the
+// laziness test is off the critical path.  Publication as in the tagged grid kernel: the item that
+// took the row's last start ticket decides -- every other chunk of its row was claimed earlier by
+// a resident CTA that finishes it without waiting on anything, so there is no dispatch-order
+// assumption and no cycle (a CTA claims its next item only after deciding).
+template <typename E, bool GREEDY>
+__global__ void __launch_bounds__(kThreads, GREEDY ? 8 : 6) k_row_stats_persist(const Params P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ __align__(16) PartA s_all[kMaxTagNch];
+    __shared__ uint32_t s_tag, s_item;
+    __shared__ unsigned long long s_state;
+    __shared__ float s_d[2][kWarps];
+    __shared__ double s_s[2][kWarps];
+    __shared__ int s_gi[kWarps], s_f[kWarps];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nch = P.nch, kk = P.k, B = P.B;
+    const uint32_t per_pos = static_cast<uint32_t>(nch) * static_cast<uint32_t>(B);
+    const uint32_t total = per_pos * static_cast<uint32_t>(kk + 1);
+    if (P.chain) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (P.prof_ts && tid == 0 && blockIdx.x == 0) prof_min(P.prof_ts);
+    // tid 0 keeps the prefetched next item and its request's state word in registers
+    uint32_t nxt = 0;
+    unsigned long long nst = 0ull;
+    auto state_of = [&](uint32_t it) -> unsigned long long {
+        const uint32_t jj = it / per_pos, bb = (it / static_cast<uint32_t>(nch)) % static_cast<uint32_t>(B);
+        return jj ? ld_relaxed_u64(P.state + bb) : 0ull;
+    };
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        s_tag = (ld_relaxed_u32(P.epoch) + 1u) | 0x80000000u;
+        nxt = atomicAdd(P.work, 1u);
+        if (nxt < total) nst = state_of(nxt);
+    }
+    uint32_t ph0 = 0, ph1 = 0;
+    while (true) {
+        if (tid == 0) {
+            s_item = nxt;
+            s_state = nst;
+            nxt = atomicAdd(P.work, 1u);                      // claim the following item
+        }
+        __syncthreads();
+        const uint32_t item = s_item;
+        if (item >= total) break;
+        const int c = static_cast<int>(item % static_cast<uint32_t>(nch));
+        const int b = static_cast<int>((item / static_cast<uint32_t>(nch)) % static_cast<uint32_t>(B));
+        const int j = static_cast<int>(item / per_pos);
+        const uint32_t m = static_cast<uint32_t>(s_state >> 32);
+        if (tid == 0 && nxt < total) nst = state_of(nxt);    // (consumed at the next item)
+        if (m & ((1u << j) - 1u)) continue;                   // the request stopped below j
+        const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
+        const int c0 = c * P.CH;
+        const int len = min(P.CH, P.V - c0);
+        const bool load_q = !GREEDY && j < kk && P.qmeta == nullptr;
+        const E* gp = static_cast<const E*>(P.p) + static_cast<int64_t>(pos) * P.ld_p + c0;
+        const E* gq = load_q ? static_cast<const E*>(P.q) + (static_cast<int64_t>(b) * kk + j) * P.ld_q + c0
+                             : nullptr;
+        E* sp = reinterpret_cast<E*>(smem);
+        E* sq = sp + P.CH;
+        const uint32_t bytes = static_cast<uint32_t>(len) * sizeof(E);
+        const uint32_t bulk = bytes & ~15u;
+        uint32_t tk = 0;
+        if (tid == 0) {
+            // generic-proxy reads of the previous item precede this async-proxy write (WAR)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive_expect_tx(&bar[0], bulk);
+            if (bulk) bulk_g2s(sp, gp, bulk, &bar[0]);
+            tk = ticket_relaxed(P.ticketA + pos);              // start ticket of the row
+        } else if (tid == 32 && load_q) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive_expect_tx(&bar[1], bulk);
+            if (bulk) bulk_g2s(sq, gq, bulk, &bar[1]);
+        }
+        const bool tail = bulk != bytes;
+        if (tail) {
+            for (int i = static_cast<int>(bulk / sizeof(E)) + tid; i < len; i += kThreads) {
+                sp[i] = gp[i];
+                if (load_q) sq[i] = gq[i];
+            }
+            __syncthreads();
+        }
+        const int x = (j < kk) ? P.ids[static_cast<size_t>(b) * kk + j] : -1;
+        const PartA pa = slice_partial<E, GREEDY>(P, sp, sq, c0, len, load_q, x, bar, ph0, ph1, s_d,
+                                                  s_s, s_gi, s_f);
+        ph0 ^= 1u;
+        if (load_q) ph1 ^= 1u;
+        if (warp != 0) continue;
+        const uint32_t tag = s_tag;
+        tk = __shfl_sync(0xFFFFFFFFu, tk, 0);
+        if (tk != static_cast<uint32_t>(nch - 1)) {           // plain tagged stores
+            if (lane == 0) write_tagged(P, pos, c, pa, tag);
+            continue;
+        }
+        // the row's decider: every other chunk of the row was claimed (and started) before
+        if (lane == 0) s_all[c] = pa;
+        bool ok = true;
+        for (int cc = lane; cc < nch; cc += 32) {
+            if (cc == c) continue;
+            PartA a;
+            ok = spin_until([&] { return read_tagged(P, pos, cc, tag, a); }, 10) && ok;
+            s_all[cc] = a;
+        }
+        ok = __all_sync(0xFFFFFFFFu, ok);
+        __syncwarp();
+        Comb C = combine_parts<GREEDY, true>(s_all, nch, lane);
+        if (!ok) C.flags |= kPartProtocol;
+        if (lane == 0) decide<GREEDY>(P, b, j, x, C);
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // Kernel B (one CTA per request): residual (or bonus) inverse-CDF sample at the stop position L.
 //
@@ -1240,8 +1377,10 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
     // programmatic dependent launch: wait until every decision of k_row_stats is visible
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (P.prof_ts && tid == 0 && blockIdx.x < 8) prof_min(P.prof_ts + 1);
-    if (P.tagpub && tid == 0 && blockIdx.x == 0)
+    if (P.tagpub && tid == 0 && blockIdx.x == 0) {
         P.epoch[0] += 1u;   // k_row_stats is complete: the next call tags with a new value
+        *P.work = 0u;       // (the persistent form's claim counter)
+    }
     // the next call's k_row_stats may be scheduled now (it waits for this grid to complete)
     if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
     const uint32_t mask = static_cast<uint32_t>(__ldcg(P.state + b) >> 32);
@@ -1517,8 +1656,10 @@ __global__ void __launch_bounds__(kThreads) k_sample_chunked(const Params P) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (P.prof_ts && tid == 0 && blockIdx.x < 8 && blockIdx.y == 0 && blockIdx.z == 0)
         prof_min(P.prof_ts + 1);
-    if (P.tagpub && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+    if (P.tagpub && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
         P.epoch[0] += 1u;   // k_row_stats is complete: the next call tags with a new value
+        *P.work = 0u;
+    }
     // the next call's k_row_stats may be scheduled now (it waits for this grid to complete)
     if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
     if (b >= P.B) return;
@@ -1557,8 +1698,10 @@ __global__ void __launch_bounds__(kThreads) k_sample_chunked(const Params P) {
 __global__ void k_finalize_greedy(const Params P) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (P.prof_ts && threadIdx.x == 0 && blockIdx.x < 8) prof_min(P.prof_ts + 1);
-    if (P.tagpub && threadIdx.x == 0 && blockIdx.x == 0)
+    if (P.tagpub && threadIdx.x == 0 && blockIdx.x == 0) {
         P.epoch[0] += 1u;   // k_row_stats is complete: the next call tags with a new value
+        *P.work = 0u;
+    }
     if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= P.B) return;
@@ -1606,8 +1749,10 @@ __global__ void k_trace(const RowStat* rowstat, const double* rres, const int32_
 // Row statistics only (sd_draft_qmeta): the second kernel just resets the workspace words.
 __global__ void k_reset(const Params P) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (P.tagpub && threadIdx.x == 0 && blockIdx.x == 0)
+    if (P.tagpub && threadIdx.x == 0 && blockIdx.x == 0) {
         P.epoch[0] += 1u;   // k_row_stats is complete: the next call tags with a new value
+        *P.work = 0u;
+    }
     if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= P.B) return;
@@ -1705,7 +1850,42 @@ static void launch_stats_cl(const Params& P, cudaStream_t st) {
     cudaLaunchKernelEx(&cfg, k_row_stats<E, G, CL, TAG>, P);
 }
 template <typename E, bool G>
+static void launch_stats_persist(const Params& P, cudaStream_t st) {
+    static std::atomic<int> cache[64];   // resident CTAs per device (SMs x occupancy)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int n = cache[dev & 63].load(std::memory_order_relaxed);
+    if (n == 0) {
+        int sms = 0, occ = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_row_stats_persist<E, G>, kThreads,
+                                                      (G ? 1 : 2) * static_cast<size_t>(kMaxChunkBytes));
+        n = sms * (occ > 0 ? occ : 1);
+        cache[dev & 63].store(n, std::memory_order_relaxed);
+    }
+    const long long items = static_cast<long long>(P.nch) * P.B * (P.k + 1);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(items < n ? items : n));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = (G ? 1 : 2) * static_cast<size_t>(P.CH) * sizeof(E);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    int na = 0;
+    if (P.chain) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, k_row_stats_persist<E, G>, P);
+}
+template <typename E, bool G>
 static void launch_stats(const Params& P, cudaStream_t st) {
+    if (P.tagpub && P.persist) {   // (tagged rows, persistent CTAs)
+        launch_stats_persist<E, G>(P, st);
+        return;
+    }
     if (P.tagpub) {   // (tagged partials: rows of 2..64 chunks without clusters)
         launch_stats_cl<E, G, 1, true>(P, st);
         return;

@@ -229,7 +229,7 @@ def test_gpu_monte_carlo_matches_exact_outcome():
 
 
 @pytest.mark.parametrize("env,want", [
-    ({"STARSD_FUSE": "0"}, ("two_launch", 0)),              # every sampling task in the tail
+    ({"STARSD_PERSIST": "1"}, ("two_launch", 0)),           # resident CTAs claiming work items
     ({"STARSD_ROWCLUSTER": "1"}, ("two_launch", 0)),        # cluster-free k_row_stats
     ({"STARSD_ROWCLUSTER": "-8"}, ("two_launch", 8)),       # clusters of 8 on every row (G > 1)
     ({"STARSD_ROWCLUSTER": "-2"}, ("two_launch", 2)),
