@@ -103,7 +103,9 @@ typedef struct {
  *   out_status    device, [B] int32 fault bitmask, or NULL
  *   workspace     device, >= sd_verify_workspace_size() bytes, 16-byte aligned, zero-filled
  *                 once before its first use.  Every call leaves the zero region of its shape
- *                 zeroed again (word 0 excepted: a call counter the kernels keep); the library
+ *                 zeroed again (words 0 and 1 excepted: 32-bit counters the kernels keep -- word
+ *                 0 counts calls, word 1 counts requests whose residual sample was taken inside
+ *                 the statistics kernel by fused sampling chunk tasks; both wrap); the library
  *                 remembers, per workspace pointer in this process, the layout of the last call
  *                 it enqueued there, and a call of another shape (batch, k, vocab, dtype, T == 0
  *                 or not) first zero-fills the union of both zero regions on `stream` (a

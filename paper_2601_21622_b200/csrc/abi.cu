@@ -170,6 +170,15 @@ static void fill_params(Params& P, const sd_shape* shape, int esz, float tempera
     P.esz = esz;
     static const int persist = env_flag("STARSD_PERSIST", 0);   // A/B knob
     P.persist = persist ? 1 : 0;
+    P.claimed = reinterpret_cast<unsigned long long*>(ws + w.claimed);
+    // fused sampling: chunks of exactly one 32-segment block (16 KB), at most 63 of them per row
+    // (opt-in: measured slower at c3 -- the stop rows are L2-cold one position wave later,
+    // profiles/README.md r02)
+    static const int fs = env_flag("STARSD_FUSED_SAMPLE", 0);   // A/B knob
+    P.fsample = (fs && !greedy && !P.persist && P.k >= 1 && P.CH * esz == kMaxChunkBytes &&
+                 P.nch <= 63) ? 1 : 0;
+    static const int rg = env_flag("STARSD_RGROUP", 0);          // A/B knob
+    P.rgroup = rg > 0 ? rg : 0;
 }
 
 }  // namespace sd

@@ -284,6 +284,17 @@ __device__ __forceinline__ void write_outputs(const Params& P, int b, int L, int
     if (P.out_status) P.out_status[b] = status;
 }
 
+// Leave request b's words of the workspace's zero region zeroed for the next call (one thread,
+// after every CTA of k_row_stats is complete).
+__device__ __forceinline__ void reset_request(const Params& P, int b) {
+    P.state[b] = 0ull;
+    for (int i = 0; i <= P.k; ++i) P.ticketA[static_cast<size_t>(b) * (P.k + 1) + i] = 0u;
+    if (P.fsample) {
+        P.ticketB[b] = 0u;
+        P.claimed[b] = 0ull;
+    }
+}
+
 // Combination of n slice partials (fp64, exact 2^(D_c - D) rescales); warp-collective, the
 // result is valid in every lane.  SHARED: the partials sit in this CTA's shared memory (cluster
 // leader, tagged decider), else in global memory written by other CTAs of this launch.
@@ -642,6 +653,119 @@ __device__ __forceinline__ float resid_scaled(uint4 up, uint4 uq, int valid, flo
     for (int u = 1; u < VEC; ++u) sr = __fadd_rn(sr, r[u]);
     return sr;
 }
+// ---- inverse CDF over on-chip / published masses (k_sample_req and the fused chunk tasks share
+// these, so both take bit-identical decisions) -------------------------------------------------
+// Levels 1 and 2 (one warp): blocks of 32 segments -> segment, first x with C(x) > theta (C-9),
+// theta = u24(w_y) * total.  blk(i): mass of block i < nblk; seg(i): mass of segment i < nseg (a
+// block's mass is the warp tree sum of its 32 segment masses).  Returns the total (every lane);
+// when it is > 0, *sgsel and *th2 (every lane) are the segment found and theta's remainder in it.
+template <typename FB, typename FS>
+__device__ __forceinline__ double cdf_search_blocks(FB blk, FS seg, int nblk, int nseg, uint32_t w_y,
+                                                    int lane, int* sgsel, double* th2) {
+    double carry = 0.0;   // level 1: blocks -- warp scans with a carry
+    for (int base = 0; base < nblk; base += 32) {
+        double v = base + lane < nblk ? blk(base + lane) : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
+            if (lane >= o) v = __dadd_rn(v, a);
+        }
+        carry = __dadd_rn(carry, __shfl_sync(0xFFFFFFFFu, v, 31));
+    }
+    const double tot = carry;
+    if (!(tot > 0.0)) return tot;
+    const double theta = unit24(w_y) * tot;
+    int bsel = -1, blast = 0;
+    double run = 0.0, th = INFINITY;
+    for (int base = 0; base < nblk && bsel < 0; base += 32) {
+        const double m = base + lane < nblk ? blk(base + lane) : 0.0;
+        double v = m;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
+            if (lane >= o) v = __dadd_rn(v, a);
+        }
+        v = __dadd_rn(run, v);
+        const unsigned h = __ballot_sync(0xFFFFFFFFu, base + lane < nblk && v > theta);
+        const unsigned pm = __ballot_sync(0xFFFFFFFFu, base + lane < nblk && m > 0.0);
+        if (pm) blast = base + 31 - __clz(pm);
+        if (h) {
+            const int l = __ffs(h) - 1;
+            double e = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+            if (lane == 0) e = run;
+            bsel = base + l;
+            th = theta - __shfl_sync(0xFFFFFFFFu, e, l);
+        }
+        run = __shfl_sync(0xFFFFFFFFu, v, 31);
+    }
+    if (bsel < 0) bsel = blast;                  // rounding: last block with mass
+    // level 2: the block's 32 segments
+    const int sgi = bsel * 32 + lane;
+    const double m = sgi < nseg ? seg(sgi) : 0.0;
+    double v = m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        if (lane >= o) v = __dadd_rn(v, a);
+    }
+    const unsigned h = __ballot_sync(0xFFFFFFFFu, sgi < nseg && v > th);
+    const unsigned pm = __ballot_sync(0xFFFFFFFFu, sgi < nseg && m > 0.0);
+    const int ls = h ? __ffs(h) - 1 : (pm ? 31 - __clz(pm) : 0);
+    double e = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+    if (lane == 0) e = 0.0;
+    *th2 = h ? th - __shfl_sync(0xFFFFFFFFu, e, ls) : INFINITY;
+    *sgsel = bsel * 32 + ls;
+    return tot;
+}
+
+// Level 3 (one warp): re-read segment sgsel of the row (p, and q when rho >= 0) from global
+// memory, recompute its scaled terms exactly as the mass pass did, scan, find the lane and the
+// token (clamps: C-9).  The token in every lane.
+template <typename E>
+__device__ __forceinline__ int32_t cdf_search_segment(const E* gp, const E* gq, int sgsel, double th2,
+                                                      int V, int nvv, float c2, float nDp, float nDq,
+                                                      float rho, int lane) {
+    constexpr int VEC = Elt<E>::VEC;
+    constexpr int SEGV = 32;
+    const int g = sgsel * SEGV + lane;
+    const int valid = min(VEC, max(0, V - g * VEC));
+    uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
+    if (g < nvv) {
+        up = __ldcg(reinterpret_cast<const uint4*>(gp) + g);
+        if (rho >= 0.0f) uq = __ldcg(reinterpret_cast<const uint4*>(gq) + g);
+    }
+    float r[VEC];
+    const float sr = resid_scaled<E>(up, uq, g < nvv - 1 ? VEC : valid, c2, nDp, nDq, rho, r);
+    double v = static_cast<double>(sr);
+    const float mine = sr;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        if (lane >= o) v = __dadd_rn(v, a);
+    }
+    const unsigned hit = __ballot_sync(0xFFFFFFFFu, v > th2);
+    const unsigned posm = __ballot_sync(0xFFFFFFFFu, mine > 0.0f);
+    const int ls = hit ? __ffs(hit) - 1 : (posm ? 31 - __clz(posm) : 0);
+    double ex = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+    if (lane == 0) ex = 0.0;
+    int fe = -1;
+    if (lane == ls) {
+        const double th3 = hit ? th2 - ex : INFINITY;
+        int lastpos = -1;
+        float cum = 0.0f;
+#pragma unroll
+        for (int e2 = 0; e2 < VEC; ++e2) {
+            const float te = r[e2];
+            if (te > 0.0f) lastpos = e2;
+            cum = e2 == 0 ? te : __fadd_rn(cum, te);
+            if (fe < 0 && static_cast<double>(cum) > th3) fe = e2;
+        }
+        if (fe < 0) fe = lastpos >= 0 ? lastpos : 0;   // rounding: clamp (C-9)
+    }
+    fe = __shfl_sync(0xFFFFFFFFu, fe, ls);
+    return (sgsel * SEGV + ls) * VEC + fe;
+}
+
 // inclusive Kogge-Stone scan of (R, P) pairs over the lanes (fixed association)
 __device__ __forceinline__ double2 warp_scan2(double2 v, int lane) {
 #pragma unroll
@@ -890,6 +1014,90 @@ __device__ __forceinline__ void sample_task(const Params& P, unsigned char* smem
     }
 }
 
+// Fused sampling chunk task (k_row_stats with P.fsample; whole CTA): chunk c of request b's stop
+// row pair (p_L, q_L), L < k, staged into this CTA's shared memory -- from L2 when the row was
+// read one position wave earlier -- and reduced exactly as k_sample_req reduces it: the scaled
+// residual terms of every 16-byte vector (resid_scaled), one fp64 warp tree sum per 32-vector
+// segment, the chunk's mass (the chunk is one 32-segment block) as the warp tree sum of its
+// segment masses.  The CTA completing the request's last task runs the same inverse-CDF search
+// (cdf_search_blocks / cdf_search_segment) over the published masses, writes the outputs and sets
+// bit 63 of claimed[b]; a zero residual (C-6) is left to k_sample_req's retry.
+template <typename E>
+__device__ __forceinline__ void fused_sample_task(const Params& P, unsigned char* smem, uint64_t* bar,
+                                                  double* s_seg, int* s_last, int b, int L, int c,
+                                                  const RowStat& rs) {
+    using EL = Elt<E>;
+    constexpr int VEC = EL::VEC;
+    constexpr int SEGV = 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int kk = P.k, V = P.V, nch = P.nch;
+    const E* gp = static_cast<const E*>(P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
+    const E* gq = static_cast<const E*>(P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q;
+    const int vpc = P.CH / VEC;                        // vectors per chunk (32 segments)
+    const int nvv = (V + VEC - 1) / VEC;               // vectors of the row
+    const int v0 = c * vpc;
+    const int nvc = min(vpc, nvv - v0);                // vectors of this chunk
+    const uint32_t bytes = static_cast<uint32_t>(nvc) * 16u;   // (row strides are 16-byte padded)
+    unsigned char* sq = smem + static_cast<size_t>(P.CH) * sizeof(E);
+    if (tid == 0) {
+        mbar_arrive_expect_tx(&bar[0], bytes);
+        bulk_g2s(smem, reinterpret_cast<const uint4*>(gp) + v0, bytes, &bar[0]);
+    } else if (tid == 32) {
+        mbar_arrive_expect_tx(&bar[1], bytes);
+        bulk_g2s(sq, reinterpret_cast<const uint4*>(gq) + v0, bytes, &bar[1]);
+    }
+    const float c2 = P.c2, nDp = -rs.M_p, nDq = -rs.M_q;
+    const float rho = static_cast<float>(rs.S_p / rs.S_q);
+    mbar_wait(&bar[0], 0u);
+    mbar_wait(&bar[1], 0u);
+    const uint4* sp4 = reinterpret_cast<const uint4*>(smem);
+    const uint4* sq4 = reinterpret_cast<const uint4*>(sq);
+#pragma unroll
+    for (int i = 0; i < 32 / kWarps; ++i) {
+        const int sg = warp + i * kWarps;
+        const int gl = sg * SEGV + lane, g = v0 + gl;
+        uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
+        if (gl < nvc) {
+            up = sp4[gl];
+            uq = sq4[gl];
+        }
+        const int valid = g < nvv - 1 ? VEC : min(VEC, max(0, V - g * VEC));
+        float r[VEC];
+        const double m =
+            warp_sum(static_cast<double>(resid_scaled<E>(up, uq, valid, c2, nDp, nDq, rho, r)));
+        if (lane == 0) s_seg[sg] = m;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const double m = s_seg[lane];
+        const double t = warp_sum(m);
+        P.segtab[(static_cast<size_t>(b) * nch + c) * 32 + lane].x = m;
+        if (lane == 0) P.partB[static_cast<size_t>(b) * nch + c].R = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) *s_last = atomicAdd(P.ticketB + b, 1u) == static_cast<uint32_t>(nch - 1);
+    __syncthreads();
+    if (!*s_last || warp != 0) return;
+    __threadfence();
+    const uint4 w = verify_words(P.seed, static_cast<uint32_t>(L), P.round,
+                                 P.rid_base + static_cast<uint64_t>(b));
+    int sgsel = 0;
+    double th2 = INFINITY;
+    const double tot = cdf_search_blocks(
+        [&](int i) { return __ldcg(&P.partB[static_cast<size_t>(b) * nch + i].R); },
+        [&](int i) { return __ldcg(&P.segtab[(static_cast<size_t>(b) * nch + (i >> 5)) * 32 + (i & 31)].x); },
+        nch, (nvv + SEGV - 1) / SEGV, w.y, lane, &sgsel, &th2);
+    if (!(tot > 0.0)) return;   // C-6: k_sample_req retries with p_L
+    const int32_t tok = cdf_search_segment<E>(gp, gq, sgsel, th2, V, nvv, c2, nDp, nDq, rho, lane);
+    if (lane == 0) {
+        write_outputs(P, b, L, tok, rs.status, false);
+        P.rres[b] = tot / rs.S_p;   // (trace) mass of the distribution sampled
+        atomicOr(P.claimed + b, 1ull << 63);
+        SD_TRF(P, 8);
+    }
+}
+
 // The slice partial of one chunk (whole CTA; valid in warp 0, zx fields in lane 0): wait for the
 // bulk copies (mbarrier parities ph0 / ph1), unpack NV vectors per thread into registers, the lean
 // statistics (or argmax) per thread, warp and block reductions.
@@ -1056,24 +1264,22 @@ __global__ void __launch_bounds__(kThreads, GREEDY ? 8 : 6) k_row_stats(const Pa
     __shared__ __align__(16) PartA s_parts[CL];
     __shared__ __align__(16) PartA s_all[TAG ? kMaxTagNch : 1]; // TAG: the row's partials
     __shared__ uint32_t s_tag;
-    __shared__ int s_flag;
+    __shared__ int s_flag, s_L, s_last;
     __shared__ float s_d[2][kWarps];
     __shared__ double s_s[2][kWarps];
+    __shared__ double s_seg[GREEDY ? 1 : 32];
     __shared__ int s_gi[kWarps], s_f[kWarps];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nch = P.nch, kk = P.k;
-    // grid (chunk, request, position): blocks are scheduled x-fastest, so all requests'
-    // position 0 come first (position-major), without any integer division
-    // grid.y covers at most kGridY requests; grid.z = (k+1) * ceil(B / kGridY) (position-major)
+    // grid (chunk, request in group, group x position): blocks are scheduled x-fastest, so within
+    // a group of gridDim.y requests all position-0 rows come first (position-major), then
+    // position 1, ...; one group (gridDim.y = B) is the plain position-major order
     const int c = blockIdx.x;
-    int b = blockIdx.y, j = blockIdx.z;
-    if (P.B > kGridY) {
-        const int nb = (P.B + kGridY - 1) / kGridY;
-        b += (j % nb) * kGridY;
-        j /= nb;
-        if (b >= P.B) return;
-    }
+    const int grp = blockIdx.z / (kk + 1);
+    const int j = blockIdx.z - grp * (kk + 1);
+    const int b = grp * gridDim.y + blockIdx.y;
+    if (b >= P.B) return;
     const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
 
     const int rank = CL > 1 ? c % CL : 0;
@@ -1084,9 +1290,23 @@ __global__ void __launch_bounds__(kThreads, GREEDY ? 8 : 6) k_row_stats(const Pa
     if (P.prof_ts && tid == 0 && blockIdx.y == 0 && blockIdx.z == 0) prof_min(P.prof_ts);
     if (tid == 0) {
         SD_TR(P, 0);
+        const bool fs = !GREEDY && P.fsample && j > 0 && c < nch;
         const unsigned long long s = j ? ld_relaxed_u64(P.state + b) : 0ull;
+        const unsigned long long cl = fs ? ld_relaxed_u64(P.claimed + b) : 0ull;
         const uint32_t m = static_cast<uint32_t>(s >> 32);
         const bool skip = (m & ((1u << j) - 1u)) != 0u;
+        // fused sampling: a request settled at L < j whose chunk task c is unclaimed -- this CTA
+        // claims it (the first position wave after L normally claims every chunk)
+        int tL = -1;
+        if (fs && skip) {
+            const int L = settled_L(s, kk);
+            const unsigned long long bit = 1ull << c;
+            if (L >= 0 && !(cl & bit) && !(atomicOr(P.claimed + b, bit) & bit)) {
+                tL = L;
+                __threadfence();   // acquire: row L's rowstat, released with the state bits
+            }
+        }
+        s_L = tL;
         if (TAG) s_tag = (ld_relaxed_u32(P.epoch) + 1u) | 0x80000000u;
         s_flag = skip;
         mbar_init(&bar[0], 1);
@@ -1116,6 +1336,13 @@ __global__ void __launch_bounds__(kThreads, GREEDY ? 8 : 6) k_row_stats(const Pa
                 } else {
                     spin_until([&] { return mbar_try_wait_cluster(&s_pbar, 0); }, 2);
                 }
+            }
+        }
+        if constexpr (!GREEDY) {
+            if (s_L >= 0) {   // fused sampling chunk task c of row L
+                const RowStat rs = load_cg(P.rowstat + static_cast<size_t>(b) * (kk + 1) + s_L);
+                if (!(rs.status & kHard))
+                    fused_sample_task<E>(P, smem, bar, s_seg, &s_last, b, s_L, c, rs);
             }
         }
         return;
@@ -1383,6 +1610,13 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
     }
     // the next call's k_row_stats may be scheduled now (it waits for this grid to complete)
     if (P.chain) asm volatile("griddepcontrol.launch_dependents;");
+    if (P.fsample && (__ldcg(P.claimed + b) >> 63)) {   // sampled by k_row_stats' chunk tasks
+        if (tid == 0) {
+            atomicAdd(P.epoch + 1, 1u);   // workspace word 1: requests sampled by fused tasks
+            reset_request(P, b);
+        }
+        return;
+    }
     const uint32_t mask = static_cast<uint32_t>(__ldcg(P.state + b) >> 32);
     const int L = mask ? __ffs(mask) - 1 : kk;
     const RowStat rs = load_cg(P.rowstat + static_cast<size_t>(b) * (kk + 1) + L);
@@ -1431,7 +1665,12 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
                 // producer warp: lane 0 streams p, lane 1 streams q, each as far ahead as the ring allows
                 for (int u = 0; u < nunits; ++u) {
                     const int n = base_u + u;
-                    if (n >= kSRing) mbar_wait(&empty[n % kSRing], ((n / kSRing) & 1) ^ 1);
+                    if (n >= kSRing) {
+                        mbar_wait(&empty[n % kSRing], ((n / kSRing) & 1) ^ 1);
+                        // the consumers' generic-proxy reads of the slot precede this
+                        // async-proxy overwrite (WAR across proxies)
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    }
                     issue(n, u);   // (the retry pass re-reads units 0.. at later ring positions)
                 }
             } else {
@@ -1495,69 +1734,18 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
             }
             __syncthreads();
             if (warp == 0) {
-                // level 1: blocks (<= NW * 4 of them) -- warp scans with a carry
                 const uint4 w = verify_words(P.seed, static_cast<uint32_t>(L), P.round,
                                              P.rid_base + static_cast<uint64_t>(b));
-                double carry = 0.0;
-                for (int base = 0; base < nblk; base += 32) {
-                    double v = base + lane < nblk ? s_blk[base + lane] : 0.0;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
-                        if (lane >= o) v = __dadd_rn(v, a);
-                    }
-                    carry = __dadd_rn(carry, __shfl_sync(0xFFFFFFFFu, v, 31));
-                }
-                const double tot = carry;
+                int sgsel = 0;
+                double th2 = INFINITY;
+                const double tot = cdf_search_blocks([&](int i) { return s_blk[i]; },
+                                                     [&](int i) { return segm[i]; }, nblk, nseg,
+                                                     w.y, lane, &sgsel, &th2);
                 if (lane == 0) {
                     s_sel[1] = tot > 0.0;
                     P.rres[b] = tot / rs.S_p;   // (trace) mass of the distribution sampled
-                }
-                if (tot > 0.0) {
-                    const double theta = unit24(w.y) * tot;      // C-9: first x with C(x) > theta
-                    int bsel = -1, blast = 0;
-                    double run = 0.0, th = INFINITY;
-                    for (int base = 0; base < nblk && bsel < 0; base += 32) {
-                        const double m = base + lane < nblk ? s_blk[base + lane] : 0.0;
-                        double v = m;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
-                            if (lane >= o) v = __dadd_rn(v, a);
-                        }
-                        v = __dadd_rn(run, v);
-                        const unsigned h = __ballot_sync(0xFFFFFFFFu, base + lane < nblk && v > theta);
-                        const unsigned pm = __ballot_sync(0xFFFFFFFFu, base + lane < nblk && m > 0.0);
-                        if (pm) blast = base + 31 - __clz(pm);
-                        if (h) {
-                            const int l = __ffs(h) - 1;
-                            double e = __shfl_up_sync(0xFFFFFFFFu, v, 1);
-                            if (lane == 0) e = run;
-                            bsel = base + l;
-                            th = theta - __shfl_sync(0xFFFFFFFFu, e, l);
-                        }
-                        run = __shfl_sync(0xFFFFFFFFu, v, 31);
-                    }
-                    if (bsel < 0) bsel = blast;                  // rounding: last block with mass
-                    // level 2: the block's 32 segments
-                    const int sgi = bsel * 32 + lane;
-                    const double m = sgi < nseg ? segm[sgi] : 0.0;
-                    double v = m;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
-                        if (lane >= o) v = __dadd_rn(v, a);
-                    }
-                    const unsigned h = __ballot_sync(0xFFFFFFFFu, sgi < nseg && v > th);
-                    const unsigned pm = __ballot_sync(0xFFFFFFFFu, sgi < nseg && m > 0.0);
-                    const int ls = h ? __ffs(h) - 1 : (pm ? 31 - __clz(pm) : 0);
-                    double e = __shfl_up_sync(0xFFFFFFFFu, v, 1);
-                    if (lane == 0) e = 0.0;
-                    const double th2 = h ? th - __shfl_sync(0xFFFFFFFFu, e, ls) : INFINITY;
-                    if (lane == 0) {
-                        s_sel[0] = bsel * 32 + ls;
-                        s_th = th2;
-                    }
+                    s_sel[0] = sgsel;
+                    s_th = th2;
                 }
             }
             __syncthreads();
@@ -1572,45 +1760,7 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
         }
         // ---- level 3: re-read the found segment, scan it, find the lane and the token -------
         if (warp == 0) {
-            const int sgsel = s_sel[0];
-            const double th2 = s_th;
-            const int g = sgsel * SEGV + lane;
-            const int valid = min(VEC, max(0, V - g * VEC));
-            uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
-            if (g < nvv) {
-                up = __ldcg(reinterpret_cast<const uint4*>(gp) + g);
-                if (rp.use_q) uq = __ldcg(reinterpret_cast<const uint4*>(gq) + g);
-            }
-            float r[VEC];
-            const float sr = resid_scaled<E>(up, uq, g < nvv - 1 ? VEC : valid, c2, rp.nDp, rp.nDq, rho, r);
-            double v = static_cast<double>(sr);
-            const float mine = sr;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double a = __shfl_up_sync(0xFFFFFFFFu, v, o);
-                if (lane >= o) v = __dadd_rn(v, a);
-            }
-            const unsigned hit = __ballot_sync(0xFFFFFFFFu, v > th2);
-            const unsigned posm = __ballot_sync(0xFFFFFFFFu, mine > 0.0f);
-            const int ls = hit ? __ffs(hit) - 1 : (posm ? 31 - __clz(posm) : 0);
-            double ex = __shfl_up_sync(0xFFFFFFFFu, v, 1);
-            if (lane == 0) ex = 0.0;
-            int fe = -1;
-            if (lane == ls) {
-                const double th3 = hit ? th2 - ex : INFINITY;
-                int lastpos = -1;
-                float cum = 0.0f;
-#pragma unroll
-                for (int e2 = 0; e2 < VEC; ++e2) {
-                    const float te = r[e2];
-                    if (te > 0.0f) lastpos = e2;
-                    cum = e2 == 0 ? te : __fadd_rn(cum, te);
-                    if (fe < 0 && static_cast<double>(cum) > th3) fe = e2;
-                }
-                if (fe < 0) fe = lastpos >= 0 ? lastpos : 0;   // rounding: clamp (C-9)
-            }
-            fe = __shfl_sync(0xFFFFFFFFu, fe, ls);
-            tok = (sgsel * SEGV + ls) * VEC + fe;
+            tok = cdf_search_segment<E>(gp, gq, s_sel[0], s_th, V, nvv, c2, rp.nDp, rp.nDq, rho, lane);
             if (zero_res) status |= kZeroResidual;
         }
     }
@@ -1624,8 +1774,7 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
             ot[i] = v;
         }
         if (P.out_status) P.out_status[b] = status;
-        P.state[b] = 0ull;       // leave the workspace zeroed for the next call
-        for (int i = 0; i <= kk; ++i) P.ticketA[static_cast<size_t>(b) * (kk + 1) + i] = 0u;
+        reset_request(P, b);     // leave the workspace zeroed for the next call
     }
 }
 
@@ -1823,8 +1972,10 @@ void record_event(cudaEvent_t ev, cudaStream_t st) {
 // (dynamic shared memory is at most 2 x 16 KB: below the 48 KB default, no opt-in attribute)
 template <typename E, bool G, int CL, bool TAG = false>
 static void launch_stats_cl(const Params& P, cudaStream_t st) {
-    const int nb = (P.B + kGridY - 1) / kGridY;
-    const dim3 gridA(CL > 1 ? P.G * CL : P.nch, P.B < kGridY ? P.B : kGridY, (P.k + 1) * nb);
+    int gr = P.B < kGridY ? P.B : kGridY;            // requests per group (grid.y)
+    if (P.rgroup > 0 && P.rgroup < gr) gr = P.rgroup;
+    const int ng = (P.B + gr - 1) / gr;
+    const dim3 gridA(CL > 1 ? P.G * CL : P.nch, gr, (P.k + 1) * ng);
     const size_t sm = (G ? 1 : 2) * static_cast<size_t>(P.CH) * sizeof(E);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = gridA;

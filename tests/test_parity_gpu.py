@@ -234,6 +234,8 @@ def test_gpu_monte_carlo_matches_exact_outcome():
     ({"STARSD_ROWCLUSTER": "-8"}, ("two_launch", 8)),       # clusters of 8 on every row (G > 1)
     ({"STARSD_ROWCLUSTER": "-2"}, ("two_launch", 2)),
     ({"STARSD_PUBLISH_TICKET": "1"}, ("two_launch", 0)),   # release-ordered partials + row ticket
+    ({"STARSD_FUSED_SAMPLE": "0"}, ("two_launch", 0)),     # every request sampled by the tail
+    ({"STARSD_RGROUP": "5"}, ("two_launch", 0)),           # group-major k_row_stats grid
 ])
 def test_kernel_variants_match_the_oracle(env, want):
     """Kernel variants chosen by environment (once per process, so in a subprocess) against the

@@ -50,7 +50,9 @@ def main():
     a = ap.parse_args()
     prof = os.path.join(ROOT, "profiles")
     for cfg in a.configs:
-        rep = os.path.join(a.src, f"full_{cfg}.ncu-rep")
+        rep = os.path.join(a.src, f"{a.tag}_full_{cfg}.ncu-rep")
+        if not os.path.exists(rep):
+            rep = os.path.join(a.src, f"full_{cfg}.ncu-rep")
         if os.path.exists(rep):
             recs, units, raw = raw_metrics(rep)
             with open(os.path.join(prof, f"{a.tag}_ncu_full_{cfg}_f32_raw.csv"), "w") as f:
@@ -70,7 +72,9 @@ def main():
             with open(os.path.join(prof, f"ncu_{cfg}_f32.json"), "w") as f:
                 json.dump(summary, f, indent=1)
             print(cfg, summary)
-        lst = os.path.join(a.src, f"launches_{cfg}.csv")
+        lst = os.path.join(a.src, f"{a.tag}_launches_{cfg}.csv")
+        if not os.path.exists(lst):
+            lst = os.path.join(a.src, f"launches_{cfg}.csv")
         if os.path.exists(lst):
             shutil.copy(lst, os.path.join(prof, f"{a.tag}_launches_{cfg}_f32.csv"))
             share = defaultdict(float)
