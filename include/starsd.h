@@ -135,13 +135,20 @@ sd_status sd_verify_workspace_size(const sd_shape* shape, float temperature, siz
  *   cluster      k_row_stats cluster size (0: none); slice = logits per CTA chunk
  *   ctas         CTAs of k_row_stats; tail_ctas: CTAs of the second kernel
  *   tagged       rows publish tagged partials to a start-ticket decider (2..64 chunks per row)
+ *   options      SD_PLAN_* bits of the scheduling options in effect (environment knobs read once
+ *                per process): PIPE = k_row_pipe replaces k_row_stats
+ *                (ctas = its persistent grid), EARLY = k_sample_req launched during the last
+ *                position wave (tail_ctas includes its completion probe), FUSED = fused sampling
+ *                chunk tasks
  */
+enum { SD_PLAN_PIPE = 1, SD_PLAN_EARLY = 2, SD_PLAN_FUSED = 4 };
 enum { SD_VARIANT_TWO_LAUNCH = 1 };
 typedef struct {
     int32_t variant, launches, cluster, slice;
     int64_t ctas;
     int64_t tail_ctas;
     int32_t tagged;
+    int32_t options;
 } sd_plan;
 sd_status sd_verify_plan(const sd_shape* shape, float temperature, sd_plan* out);
 

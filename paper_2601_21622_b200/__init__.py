@@ -63,7 +63,8 @@ def plan(batch: int, k: int, vocab: int, temperature: float,
           "sd_verify_plan")
     return {"variant": _lib.VARIANT_NAMES.get(out.variant, str(out.variant)),
             "launches": out.launches, "cluster": out.cluster, "slice": out.slice,
-            "ctas": out.ctas, "tail_ctas": out.tail_ctas, "tagged": bool(out.tagged)}
+            "ctas": out.ctas, "tail_ctas": out.tail_ctas, "tagged": bool(out.tagged),
+            "options": [n for bit, n in _lib.PLAN_OPTIONS.items() if out.options & bit]}
 
 
 class Workspace:

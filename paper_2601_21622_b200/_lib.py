@@ -38,7 +38,10 @@ class Shape(ctypes.Structure):
 class Plan(ctypes.Structure):
     _fields_ = [("variant", ctypes.c_int32), ("launches", ctypes.c_int32),
                 ("cluster", ctypes.c_int32), ("slice", ctypes.c_int32), ("ctas", ctypes.c_int64),
-                ("tail_ctas", ctypes.c_int64), ("tagged", ctypes.c_int32)]
+                ("tail_ctas", ctypes.c_int64), ("tagged", ctypes.c_int32), ("options", ctypes.c_int32)]
+
+
+PLAN_OPTIONS = {1: "pipe", 2: "early", 4: "fused"}
 
 
 VARIANT_NAMES = {1: "two_launch"}

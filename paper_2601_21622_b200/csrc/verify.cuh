@@ -83,7 +83,6 @@ struct Params {
     uint32_t* ticketA;           // [B][k+1] row tickets (tagged rows: start order; else arrival)
     uint32_t* ticketB;           // [B]    sampling chunk tasks finished
     uint32_t* tailT;             // [B]    k_sample_chunked CTAs finished
-    uint32_t* work;              // [1]    persistent k_row_stats: next work item to claim
     RowStat* rowstat;            // [B][k+1]
     PartA* partA;                // [B][k+1][nch]
     PartB* partB;                // [B][nch]
@@ -103,8 +102,6 @@ struct Params {
     int32_t chain;               // k_row_stats launched as a programmatic dependent of whatever
                                  // kernel precedes it on the stream (griddepcontrol.wait first)
     int32_t esz;                 // bytes per logit
-    int32_t persist;             // tagged rows run as k_row_stats_persist (resident CTAs claiming
-                                 // work items) instead of one CTA per item
     const QMeta* qmeta;          // [B][k] draft-row metadata: the q rows are then read only at the
                                  // stop position (sd_verify_qmeta); NULL: full q rows
     // fused sampling (fsample): a k_row_stats CTA of position j > L whose request is settled at L
@@ -113,6 +110,8 @@ struct Params {
     // left (the bonus position, the C-6 retry, hard faults, a request settled too late)
     int32_t fsample;
     unsigned long long* claimed; // [B] bits 0..62: chunk task c claimed; bit 63: outputs written
+    int32_t early;               // k_sample_req launched during k_row_stats' last position wave
+    int32_t pipe;                // k_row_pipe (pipelined persistent CTAs) instead of k_row_stats
     int32_t rgroup;              // k_row_stats grid: requests per group (grid order: group-major,
                                  // then position, request, chunk); B = one group (position-major)
 };
@@ -143,7 +142,7 @@ inline int32_t row_cluster(int32_t nch) {
 // Workspace layout for a shape; all offsets 16-byte aligned.  The first `zero_bytes` must be
 // zero before a call and are zero again after it (word 0, the call counter, excepted).
 struct WsLayout {
-    size_t epoch, state, ticketA, ticketB, tailT, work, claimed, zero_bytes;
+    size_t epoch, state, ticketA, ticketB, tailT, claimed, zero_bytes;
     size_t rowstat, partA, partB, segtab, rres, partT, total;
 };
 
@@ -170,7 +169,6 @@ inline WsLayout ws_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
     w.ticketA = o;  o = align16(o + sizeof(uint32_t) * (size_t)B * (k + 1));
     w.ticketB = o;  o = align16(o + sizeof(uint32_t) * B);
     w.tailT = o;    o = align16(o + sizeof(uint32_t) * B);
-    w.work = o;     o = align16(o + sizeof(uint32_t));
     w.claimed = o;  o = align16(o + sizeof(unsigned long long) * B);
     w.zero_bytes = o;
     w.rowstat = o;  o = align16(o + sizeof(RowStat) * (size_t)B * (k + 1));

@@ -132,7 +132,9 @@ def test_verify_plan_default_is_two_launch_with_16kb_chunks(lib):
     assert pl["variant"] == "two_launch" and pl["launches"] == 2
     assert pl["slice"] == 4096 and pl["ctas"] == 8 * 128 * 32
     assert pl["cluster"] == 0                                  # nch = 32 > 8: cluster-free rows
-    assert pl["tagged"] and pl["tail_ctas"] == 128             # start-ticket deciders; k_sample_req
+    # start-ticket deciders; k_sample_req (one CTA per request) launched during the last position
+    # wave, plus its completion probe
+    assert pl["tagged"] and pl["tail_ctas"] == 129 and pl["options"] == ["early"]
     assert sd.plan(128, 7, 128256, 0.0)["tail_ctas"] == 1     # greedy finalize: 128 threads/CTA
     plb = sd.plan(64, 5, 32000, 0.0, torch.bfloat16)          # bf16: 8192 logits per 16 KB chunk
     assert plb["slice"] == 8192 and plb["ctas"] == 6 * 64 * 4 and plb["cluster"] == 4

@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 if [ -n "$PYTEST_FILES" ]; then
-  timeout 1500 python -m pytest $PYTEST_FILES -m gpu -q -x -p no:cacheprovider > gpurun_out/ab_pytest.log 2>&1
+  timeout ${PYTEST_TIMEOUT:-600} python -m pytest $PYTEST_FILES -m gpu -q -x -p no:cacheprovider ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/ab_pytest.log 2>&1
   echo "pytest rc=$?" >> gpurun_out/ab_pytest.log; tail -3 gpurun_out/ab_pytest.log
 fi
 CFGS=${CFGS:-"c3 c2"}
@@ -13,12 +13,14 @@ for cfg in $CFGS; do
     case $v in
       base) E="";;
       FUSED0) E="STARSD_FUSED_SAMPLE=0";;
-      PERSIST) E="STARSD_PERSIST=1";;
+      PIPE) E="STARSD_PIPE=1";;
+      PIPE2) E="STARSD_PIPE=2";;
+      EARLY0) E="STARSD_EARLY=0";;
       TICKET) E="STARSD_PUBLISH_TICKET=1";;
       RG*) E="STARSD_RGROUP=${v#RG}";;
       *) E="$v";;
     esac
-    env $E timeout 400 python bench.py --config $cfg --no-cpu --no-e2e --steps 1000 $BENCH_ARGS > gpurun_out/ab_${cfg}_$v.json 2> gpurun_out/ab_${cfg}_$v.err
+    env $E timeout ${BENCH_TIMEOUT:-150} python bench.py --config $cfg --no-cpu --no-e2e --steps 1000 $BENCH_ARGS > gpurun_out/ab_${cfg}_$v.json 2> gpurun_out/ab_${cfg}_$v.err
     python - <<PY
 import json
 try:

@@ -84,7 +84,7 @@ k_probe(const char* __restrict__ src, size_t total, size_t per_cta, int cb, int 
             // 32 KB chunk: 8 vectors per thread into registers, release, then max + sum of ex2
             float4 x[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) x[i] = v[warp * 32 + lane + i * 256];
+            for (int i = 0; i < 8; ++i) x[i] = i < cb / 4096 ? v[warp * 32 + lane + i * 256] : make_float4(0.f, 0.f, 0.f, 0.f);
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(empty + s)) : "memory");
             float m = -INFINITY;
@@ -133,19 +133,18 @@ int main() {
     const size_t per_cta = 24ull << 20;   // 24 MB per CTA (~3.4 GB total)
     cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     printf("SMs=%d grid=%d\n", sms, grid);
-    for (int threads : {288, 512})
-    for (int clus : {1, 8})
-    for (int stages : {4, 6}) {
-        const int cb = 32768, nprod = 2, compute = 1, pattern = 1;
+    // sweep: copy size x ring depth x issuing threads (192 KB ring, 1 CTA per SM, stats consumers)
+    for (int pattern : {0, 1})
+    for (int cb : {16384, 32768})
+    for (int nprod : {1, 2, 4, 12}) {
+        const int stages = 196608 / cb, threads = 288, compute = 1;
+        if (nprod > stages) continue;
         const size_t smem = (size_t)stages * cb + 2 * (stages + 1) * 8;
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(clus == 8 ? 120 : grid);
+        cfg.gridDim = dim3(sms);
         cfg.blockDim = dim3(threads);
         cfg.dynamicSmemBytes = smem;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = clus; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-        cfg.attrs = at; cfg.numAttrs = 1;
+        cfg.numAttrs = 0;
         const int g = cfg.gridDim.x;
         auto launch = [&] { cudaLaunchKernelEx(&cfg, k_probe, (const char*)src, total, per_cta / cb, cb, stages, nprod, pattern, out, ic, compute); };
         launch(); cudaDeviceSynchronize();
@@ -154,7 +153,7 @@ int main() {
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b);
         cudaError_t e = cudaGetLastError();
-        printf("threads=%d cluster=%d grid=%d stages=%d compute=1 2 producers 32 KB: %7.1f GB/s (%6.1f GB/s per CTA) %s\n", threads, clus, g, stages,
+        printf("pattern=%d copy=%d KB stages=%d issuers=%d: %7.1f GB/s (%6.1f GB/s per SM) %s\n", pattern, cb / 1024, stages, nprod,
                (double)g * per_cta * 3 / (ms * 1e-3) / 1e9, (double)per_cta * 3 / (ms * 1e-3) / 1e9, e ? cudaGetErrorString(e) : "");
     }
     for (int pattern : {0, 1}) {
