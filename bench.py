@@ -8,11 +8,11 @@ synthetic logits that is already resident in HBM.  The default workload is BASEL
 configs[2] -- the Llama-3 shape north_star's target is quoted on (V=128256, k=7, B=128 per
 verifier, T=1, fp32, kappa=30).  Eight distinct batches (7.9 GB > the 126 MB L2) are rotated so
 no step reads L2-resident inputs of the previous one.
-K steps are captured in one CUDA graph and timed with CUDA events on the launching stream (a
-second graph of the same K steps with profiling events around k_row_stats gives the roofline's
-kernel time);
-multi-GPU runs (torchrun) run one independent verifier per GPU (the verify step shards by
-request; no data-path collective) and report the max time over ranks.
+K steps are captured in one CUDA graph and timed with CUDA events on the launching stream (device
+timestamps inside the same graph give the dominant kernel's span for the roofline).
+Multi-GPU runs (torchrun, N > 1) run the star of PAPER.md Alg. 1: rank 0 drafts, ranks 1..N-1
+verify over NCCL (--mode dp: independent verifiers instead); --star-loopback N emulates a 1 -> N
+star on one GPU.  Times are the max over ranks.
 
 Printed: one JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
 """
@@ -549,9 +549,11 @@ def run_star(args):
             torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         tokens = float(tok_acc.item())
+        alg = 0.0                                            # verifier-side algorithmic bytes
         for v, Ls in Lhost.items():
             for Lt in Ls:
                 h.observe(v, Lt.numpy())
+                alg += float(algorithmic_bytes(Lt.numpy(), V, k, esize(args.dtype), T == 0.0).sum())
         st = h.stats()
         try:
             pred = h.predict(args.o_alone)
@@ -611,9 +613,18 @@ def run_star(args):
                      "predicted": pred,
                      "closed_form_busy": (min(1.0, nver * S_ms / (S_ms + Z_ms))
                                           if S_ms and Z_ms is not None else None)},
-            "roofline": None,
+            # the verifiers' HBM roofline averaged over the window: algorithmic bytes of every
+            # verify (realized L) / window / verifier GPUs (loopback: one GPU plays
+            # all roles, so the fraction also carries the draft's GEMMs and sampling)
+            "roofline": {"bound": "hbm", "kernel": "k_row_stats (verifier side, window average)",
+                         "achieved": alg / (ms / 1000.0) / 1e9 / (1 if loop else nver),
+                         "peak": load_peaks()[0], "peak_kind": load_peaks()[1], "unit": "GB/s",
+                         "frac": alg / (ms / 1000.0) / 1e9 / (1 if loop else nver) / load_peaks()[0],
+                         "traffic": None, "alg_bytes_per_round": alg / max(1, K)},
             "e2e": None,
-            "gpu_launches": None,
+            # our kernels in the window: per verifier-round, sd_verify (2) on the verifier and
+            # sd_draft_sample (2, + the q-metadata gather with the lazy payload) on the draft
+            "gpu_launches": K * nver * slots * (4 + (1 if args.payload == "qmeta" else 0)),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
