@@ -1,19 +1,32 @@
-# One GPU measurement round: smoke, gpu tests, bench lines, ncu launch lists + full captures.
-# Run on the box: gpurun --timeout 3000 -- "bash tools/gpu_round.sh"
+# One GPU measurement round: smoke, GPU tests, bench lines, ncu launch lists + full captures,
+# compute-sanitizer.  Every step has its own timeout (sum well below the gpurun limit).
+#   gpurun --timeout 2700 -- "TAG=r02_v3 bash tools/gpu_round.sh"
 mkdir -p gpurun_out
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > gpurun_out/smoke.log 2>&1
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
-for cfg in c3 c2g c3g; do
-  timeout 600 python bench.py --config $cfg --no-cpu > gpurun_out/bench_$cfg.json 2> gpurun_out/bench_$cfg.err
+TAG=${TAG:-r02}
+O=gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/nvsmi.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > $O/${TAG}_smoke.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/${TAG}_pytest_gpu.log
+tail -2 $O/${TAG}_pytest_gpu.log
+timeout 300 python bench.py > $O/${TAG}_bench_c3.json 2> $O/${TAG}_bench_c3.err
+timeout 240 python bench.py --config c2 > $O/${TAG}_bench_c2.json 2> $O/${TAG}_bench_c2.err
+timeout 240 python bench.py --config c3g --no-cpu > $O/${TAG}_bench_c3g.json 2> $O/${TAG}_bench_c3g.err
+timeout 240 python bench.py --config c3 --dtype bf16 --no-cpu > $O/${TAG}_bench_c3_bf16.json 2> $O/${TAG}_bench_c3_bf16.err
+timeout 240 python bench.py --config c2 --dtype bf16 --no-cpu > $O/${TAG}_bench_c2_bf16.json 2> $O/${TAG}_bench_c2_bf16.err
+STARSD_PIPE=1 timeout 240 python bench.py --no-cpu --no-e2e > $O/${TAG}_bench_c3_pipe.json 2> $O/${TAG}_bench_c3_pipe.err
+timeout 240 python bench.py --impl reference --steps 3 --warmup 1 > $O/${TAG}_bench_ref.json 2> $O/${TAG}_bench_ref.err
+timeout 240 python bench.py --star-loopback 3 --steps 10 --warmup 3 > $O/${TAG}_bench_star_loop3_full.json 2> $O/${TAG}_bench_star_full.err
+timeout 240 python bench.py --star-loopback 3 --steps 10 --warmup 3 --payload qmeta > $O/${TAG}_bench_star_loop3_qmeta.json 2> $O/${TAG}_bench_star_qmeta.err
+for cfg in c3 c2 c3g; do
+  timeout 240 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_row|k_sample|k_final" --csv --log-file $O/${TAG}_launches_${cfg}.csv python tools/profile_run.py --config $cfg --calls 30 > /dev/null 2>&1
 done
-timeout 600 python bench.py --config c2 --dtype bf16 --no-cpu > gpurun_out/bench_c2_bf16.json 2> gpurun_out/bench_c2_bf16.err
-timeout 600 python bench.py --config c3 --dtype bf16 --no-cpu > gpurun_out/bench_c3_bf16.json 2> gpurun_out/bench_c3_bf16.err
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_row|k_sample|k_final" --csv --log-file gpurun_out/launches_c2.csv python tools/profile_run.py --config c2 --calls 30 > /dev/null 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_row|k_sample|k_final" --csv --log-file gpurun_out/launches_c3.csv python tools/profile_run.py --config c3 --calls 30 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_row_stats|k_sample" -s 10 -c 2 -f -o gpurun_out/full_c2 python tools/profile_run.py --config c2 --calls 16 > gpurun_out/ncu_full_c2.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_row_stats|k_sample" -s 10 -c 2 -f -o gpurun_out/full_c3 python tools/profile_run.py --config c3 --calls 16 > gpurun_out/ncu_full_c3.log 2>&1
-ls -la gpurun_out
+for cfg in c3 c2; do
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:"k_row_stats|k_sample" -s 4 -c 2 -f -o $O/${TAG}_full_${cfg} python tools/profile_run.py --config $cfg --calls 8 --nbatch 2 > $O/${TAG}_ncu_full_${cfg}.log 2>&1
+done
+for tool in memcheck racecheck synccheck; do
+  timeout 400 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize_run.py > $O/${TAG}_sanitizer_${tool}.log 2>&1
+  echo "rc=$?" >> $O/${TAG}_sanitizer_${tool}.log
+done
+tail -3 $O/${TAG}_sanitizer_*.log
+for f in $O/${TAG}_bench_*.json; do echo "$f"; cut -c1-400 "$f"; done
