@@ -261,11 +261,14 @@ pl = sd.plan(128, 7, 128256, 1.0)
 assert pl["variant"] == want[0], pl
 if want[1] is not None:
     assert pl["cluster"] == want[1], pl
-for (V, k, B, T, ld) in [(32000, 5, 64, 1.0, 32000), (32000, 5, 64, 0.0, 32000), (1003, 3, 50, 1.0, 1004),
-                         (12345, 6, 9, 0.5, 12348), (128256, 3, 6, 1.0, 128256), (128256, 3, 6, 0.0, 128256)]:
-    d = make_batch(V=V, k=k, B=B, T=max(T, 1e-3), kappa=10.0, seed=V + k, ld=ld)
+for (V, k, B, T, ld, dt) in [(32000, 5, 64, 1.0, 32000, "f32"), (32000, 5, 64, 0.0, 32000, "f32"),
+                             (1003, 3, 50, 1.0, 1004, "f32"), (12345, 6, 9, 0.5, 12348, "f32"),
+                             (128256, 3, 6, 1.0, 128256, "f32"), (128256, 3, 6, 0.0, 128256, "f32"),
+                             (128256, 4, 5, 1.0, 128256, "bf16"), (100000, 2, 7, 1.0, 100000, "bf16")]:
+    d = make_batch(V=V, k=k, B=B, T=max(T, 1e-3), kappa=10.0, seed=V + k, ld=ld, dtype=dt)
     dev = torch.device("cuda:0")
-    p = torch.from_numpy(d["p"]).to(dev); q = torch.from_numpy(d["q"]).to(dev); ids = torch.from_numpy(d["ids"]).to(dev)
+    tdev = lambda a: (torch.from_numpy(a).view(torch.bfloat16) if a.dtype == np.uint16 else torch.from_numpy(a)).to(dev)
+    p = tdev(d["p"]); q = tdev(d["q"]); ids = torch.from_numpy(d["ids"]).to(dev)
     L, tok, st = sd.verify(p, q if T > 0 else None, ids, T, seed=1234, round=5, request_id_base=1000, vocab=V)
     torch.cuda.synchronize()
     gpu = (L.cpu().numpy(), tok.cpu().numpy(), st.cpu().numpy())
