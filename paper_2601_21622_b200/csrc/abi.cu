@@ -144,7 +144,7 @@ static void fill_params(Params& P, const sd_shape* shape, int esz, float tempera
     P.V = shape->vocab;
     P.ld_p = shape->ld_p ? shape->ld_p : shape->vocab;
     P.ld_q = shape->ld_q ? shape->ld_q : shape->vocab;
-    chunking(P.V, esz, &P.nch, &P.CH);
+    chunking(P.V, esz, &P.nch, &P.CH, rs_chunk_bytes(greedy, esz));
     P.CL = row_cluster(P.nch);
     P.G = (P.nch + P.CL - 1) / P.CL;
     P.nseg = P.CH / (32 * (kVecBytes / esz));
@@ -172,10 +172,10 @@ static void fill_params(Params& P, const sd_shape* shape, int esz, float tempera
     // (opt-in: measured slower at c3 -- the stop rows are L2-cold one position wave later,
     // profiles/README.md r02)
     static const int fs = env_flag("STARSD_FUSED_SAMPLE", 0);   // A/B knob
-    P.fsample = (fs && !greedy && P.k >= 1 && P.CH * esz == kMaxChunkBytes &&
+    P.fsample = (fs && !greedy && P.k >= 1 && P.CH * esz == 16 * 1024 &&
                  P.nch <= 63) ? 1 : 0;
     static const int pipe = env_flag("STARSD_PIPE", 0);         // A/B knob
-    P.pipe = (pipe && P.nch >= 9 && P.nch <= kMaxTagNch) ? (pipe == 2 ? 2 : 1) : 0;
+    P.pipe = (pipe && P.nch >= 9 && P.nch <= kMaxTagNch && P.CH * esz <= kMaxChunkBytes) ? (pipe == 2 ? 2 : 1) : 0;
     if (P.pipe) {
         P.tagpub = 1;   // (tagged partials; the second kernel advances the call counter)
         P.fsample = 0;
@@ -452,7 +452,7 @@ sd_status sd_verify_plan(const sd_shape* shape, float temperature, sd_plan* out)
     if (!out) return fail(SD_ERR_INVALID_ARGUMENT, "out is NULL");
     *out = sd_plan{};
     int32_t nch, CH;
-    chunking(shape->vocab, esz, &nch, &CH);
+    chunking(shape->vocab, esz, &nch, &CH, rs_chunk_bytes(temperature == 0.0f, esz));
     out->variant = SD_VARIANT_TWO_LAUNCH;
     out->launches = 2;
     out->slice = CH;

@@ -11,7 +11,12 @@ constexpr int kThreads = 256;            // threads per CTA (8 warps)
 constexpr int kWarps = kThreads / 32;
 constexpr int kVecBytes = 16;            // one 128-bit smem/global vector per thread per tile
 constexpr int kTileBytes = kThreads * kVecBytes;   // 4 KB of one row per tile
-constexpr int kMaxChunkBytes = 16 * 1024;          // one CTA owns <= 16 KB of a row (measured best of 8/16/32 KB)
+constexpr int kMaxChunkBytes = 16 * 1024;          // one CTA owns <= 16 KB of a row ...
+// ... except greedy fp32 rows (p only): 32 KB slices, 6 CTAs per SM by shared memory (measured:
+// c3g 54.1 -> 45.8 us; sampled and bf16 rows are faster at 16 KB, profiles/README.md r02)
+__host__ __device__ constexpr int rs_chunk_bytes(bool greedy, int esz) {
+    return greedy && esz == 4 ? 2 * kMaxChunkBytes : kMaxChunkBytes;
+}
 constexpr int kRowClusterDefault = 8;              // see row_cluster()
 constexpr int kMaxTagNch = 64;                     // tagged partials: rows of at most 64 chunks
 
@@ -148,9 +153,11 @@ struct WsLayout {
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-inline void chunking(int32_t V, int32_t esz, int32_t* nch, int32_t* CH) {
+// (the workspace is laid out for the default 16 KB slices: the most chunks a row can have)
+inline void chunking(int32_t V, int32_t esz, int32_t* nch, int32_t* CH,
+                     int32_t chunk_bytes = kMaxChunkBytes) {
     const int64_t tile = kTileBytes / esz;                 // elements per tile
-    const int64_t chmax = kMaxChunkBytes / esz;
+    const int64_t chmax = chunk_bytes / esz;
     int64_t n = (V + chmax - 1) / chmax;
     int64_t per = (V + n - 1) / n;
     int64_t ch = (per + tile - 1) / tile * tile;

@@ -1108,7 +1108,7 @@ __device__ __forceinline__ PartA slice_partial(const Params& P, const E* sp, con
                                                double (*s_s)[kWarps], int* s_gi, int* s_f) {
     using EL = Elt<E>;
     constexpr int VEC = EL::VEC;
-    constexpr int NV = kMaxChunkBytes / kVecBytes / kThreads;   // 16-byte vectors per thread
+    constexpr int NV = rs_chunk_bytes(GREEDY, sizeof(E)) / kVecBytes / kThreads;   // vectors per thread
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // ---- registers: NV vectors of p (and q) per thread; -inf past the slice end ------------
     const int nfull = len / VEC;                 // complete vectors
@@ -1253,11 +1253,16 @@ __device__ __forceinline__ PartA slice_partial(const Params& P, const E* sp, con
 // of the row has started (and never waits on anything): it polls their tagged partials and
 // decides.  Skipping CTAs take no ticket -- a needed row (j <= L) never sees a stop below j, so
 // all its chunks take tickets; an unneeded row may end without a decider.
+// resident CTAs per SM: registers (40 / 32 per thread) with 16 KB slices; shared memory with the
+// 32 KB slices of greedy fp32 rows
+constexpr int rs_min_blocks(bool greedy, int esz) {
+    return rs_chunk_bytes(greedy, esz) > kMaxChunkBytes ? 6 : (greedy ? 8 : 6);
+}
 template <typename E, bool GREEDY, int CL, bool TAG>
-__global__ void __launch_bounds__(kThreads, GREEDY ? 8 : 6) k_row_stats(const Params P) {
+__global__ void __launch_bounds__(kThreads, rs_min_blocks(GREEDY, sizeof(E))) k_row_stats(const Params P) {
     using EL = Elt<E>;
     constexpr int VEC = EL::VEC;
-    constexpr int NV = kMaxChunkBytes / kVecBytes / kThreads;   // 16-byte vectors per thread
+    constexpr int NV = rs_chunk_bytes(GREEDY, sizeof(E)) / kVecBytes / kThreads;   // vectors per thread
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ __align__(8) uint64_t s_pbar;                    // CL > 1, leader: peer partials
@@ -2318,9 +2323,28 @@ void record_event(cudaEvent_t ev, cudaStream_t st) {
     else
         cudaEventRecord(ev, st);
 }
-// (dynamic shared memory is at most 2 x 16 KB: below the 48 KB default, no opt-in attribute)
+// k_sample_req's dynamic shared memory (ring + segment masses) needs the opt-in attribute, which
+// is per device: set it once per device (thread-safe, ADVICE r1).
+template <typename K>
+static cudaError_t ensure_smem_optin(K kernel, int bytes, std::atomic<uint64_t>& done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
+
+// (dynamic shared memory: 2 x kMaxChunkBytes at most; above the 48 KB default it needs the
+// per-device opt-in)
 template <typename E, bool G, int CL, bool TAG = false>
 static void launch_stats_cl(const Params& P, cudaStream_t st) {
+    if ((G ? 1 : 2) * rs_chunk_bytes(G, sizeof(E)) > 48 * 1024) {
+        static std::atomic<uint64_t> optin{0};
+        ensure_smem_optin(k_row_stats<E, G, CL, TAG>, (G ? 1 : 2) * rs_chunk_bytes(G, sizeof(E)), optin);
+    }
     int gr = P.B < kGridY ? P.B : kGridY;            // requests per group (grid.y)
     if (P.rgroup > 0 && P.rgroup < gr) gr = P.rgroup;
     const int ng = (P.B + gr - 1) / gr;
@@ -2349,20 +2373,6 @@ static void launch_stats_cl(const Params& P, cudaStream_t st) {
     cfg.numAttrs = na;
     cudaLaunchKernelEx(&cfg, k_row_stats<E, G, CL, TAG>, P);
 }
-// k_sample_req's dynamic shared memory (ring + segment masses) needs the opt-in attribute, which
-// is per device: set it once per device (thread-safe, ADVICE r1).
-template <typename K>
-static cudaError_t ensure_smem_optin(K kernel, int bytes, std::atomic<uint64_t>& done) {
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    const uint64_t bit = 1ull << (dev & 63);
-    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
-    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
-    return e;
-}
-
 template <typename E, bool G, int NG>
 static cudaError_t launch_stats_pipe(const Params& P, cudaStream_t st) {
     static std::atomic<uint64_t> optin{0};
@@ -2422,6 +2432,10 @@ static cudaError_t launch_sampled(const Params& P, cudaStream_t st, cudaEvent_t 
     const size_t smB = static_cast<size_t>(kSRing) * 2 * kSUnitBytes + sizeof(double) * kSMaxSeg;
     if (nseg_row <= kSMaxSeg) {
         cudaError_t e = ensure_smem_optin(k_sample_req<E>, static_cast<int>(smB), optin);
+        if (e != cudaSuccess) return e;
+    } else if (smem > 48 * 1024) {
+        static std::atomic<uint64_t> optin2{0};
+        cudaError_t e = ensure_smem_optin(k_sample_chunked<E>, static_cast<int>(smem), optin2);
         if (e != cudaSuccess) return e;
     }
     record_event(ev0, st);

@@ -135,7 +135,9 @@ def test_verify_plan_default_is_two_launch_with_16kb_chunks(lib):
     # start-ticket deciders; k_sample_req (one CTA per request) launched during the last position
     # wave, plus its completion probe
     assert pl["tagged"] and pl["tail_ctas"] == 129 and pl["options"] == ["early"]
-    assert sd.plan(128, 7, 128256, 0.0)["tail_ctas"] == 1     # greedy finalize: 128 threads/CTA
+    pg = sd.plan(128, 7, 128256, 0.0)
+    assert pg["tail_ctas"] == 1                                # greedy finalize: 128 threads/CTA
+    assert pg["slice"] == 8192 and pg["ctas"] == 8 * 128 * 16  # greedy fp32 rows: 32 KB slices
     plb = sd.plan(64, 5, 32000, 0.0, torch.bfloat16)          # bf16: 8192 logits per 16 KB chunk
     assert plb["slice"] == 8192 and plb["ctas"] == 6 * 64 * 4 and plb["cluster"] == 4
     # a cluster covers a whole row of nch <= 8 chunks (power of two, padded with empty chunks)
