@@ -128,7 +128,10 @@ def test_parity_c3_bf16():
 
 # ---------------------------------------------------------------- edge cases --------------
 @pytest.mark.parametrize("V,k,B", [(2, 1, 64), (8, 31, 16), (1003, 3, 50), (4097, 2, 33),
-                                   (12345, 6, 9), (32768, 1, 5)])
+                                   (12345, 6, 9), (32768, 1, 5),
+                                   # more requests than SMs: the early sampler's CTAs (and its
+                                   # completion probe) run in several waves behind k_row_stats
+                                   (4096, 2, 400), (40000, 3, 1), (70000, 1, 160)])
 def test_parity_ragged_shapes(V, k, B):
     """Vocabularies that are not multiples of the vector/tile/chunk sizes, k at its extremes."""
     ld = (V + 3) // 4 * 4          # rows 16-byte aligned
