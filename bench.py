@@ -57,6 +57,10 @@ def parse():
     ap.add_argument("--draft-hidden", type=int, default=4096)
     ap.add_argument("--o-alone", type=float, default=0.0,
                     help="standalone target tokens/ms for the N_max admission bound")
+    ap.add_argument("--batches", default="",
+                    help="star: per-verifier batch sizes, comma-separated (C4 heterogeneous star)")
+    ap.add_argument("--kappas", default="",
+                    help="star: per-verifier draft/target agreement kappa, comma-separated (C4)")
     return ap.parse_args()
 
 
@@ -468,12 +472,18 @@ def run_star(args):
         dist.init_process_group("nccl", device_id=dev)
     c = workload(args)
     V, k, B, T = c["V"], c["k"], c["B"], c["T"]
+    # per-verifier batch and agreement (C4: a heterogeneous star; default: all equal)
+    lst = lambda txt, cast, dflt: ([cast(x) for x in txt.split(",")] if txt else [dflt])  # noqa: E731
+    Bl, Kl = lst(args.batches, int, B), lst(args.kappas, float, c["kappa"] or 30.0)
+    Bv = {v: Bl[(v - 1) % len(Bl)] for v in range(1, nver + 1)}
+    Kv = {v: Kl[(v - 1) % len(Kl)] for v in range(1, nver + 1)}
+    B = max(Bv.values())                                                   # the star's max batch
     tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     npool, slots = 2, args.slots
     K, W = args.steps, max(3, args.warmup)
 
     def pool_batch(v, i):
-        return make_batch_torch(V, k, B, T, c["kappa"] or 30.0, c["seed"] + 7919 * v + i, dev,
+        return make_batch_torch(V, k, Bv[v], T, Kv[v], c["seed"] + 7919 * v + i, dev,
                                 dtype=args.dtype)
 
     ids_x = star.exchange_ids(rank, world) if not loop else None
@@ -495,8 +505,8 @@ def run_star(args):
                 del bt
         Wt = (torch.randn(args.draft_hidden, V, device=dev, dtype=torch.bfloat16) * 0.02)
         hid = torch.randn(B, args.draft_hidden, device=dev, dtype=torch.bfloat16)
-        bufs = {(v, s): (torch.empty(B, dtype=torch.int32, device=dev),
-                         torch.empty(B, k + 1, dtype=torch.int32, device=dev))
+        bufs = {(v, s): (torch.empty(Bv[v], dtype=torch.int32, device=dev),
+                         torch.empty(Bv[v], k + 1, dtype=torch.int32, device=dev))
                 for v in range(1, nver + 1) for s in range(slots)}
         drafted = {}
         tok_acc = torch.zeros((), dtype=torch.int64, device=dev)
@@ -507,7 +517,7 @@ def run_star(args):
             q = qpool[(v, pidx(r, s))]
             h.draft_begin(verifier=v)
             for _ in range(k):                                             # S(d) = d t_s
-                torch.matmul(hid, Wt)
+                torch.matmul(hid[:Bv[v]], Wt)
             ids, qm, _ = sd.draft_sample(q, T, seed=21622, round=r, request_id_base=rid(v, s),
                                          want_qmeta=args.payload == "qmeta")
             h.draft_end()
@@ -562,8 +572,8 @@ def run_star(args):
         perv = (per_v.cpu().numpy()[1:] / (ms / 1000.0)).tolist()
     else:
         ppool = {i: pool_batch(rank, i)["p"] for i in range(npool)}
-        outs = {s: (torch.empty(B, dtype=torch.int32, device=dev),
-                    torch.empty(B, k + 1, dtype=torch.int32, device=dev)) for s in range(slots)}
+        outs = {s: (torch.empty(Bv[rank], dtype=torch.int32, device=dev),
+                    torch.empty(Bv[rank], k + 1, dtype=torch.int32, device=dev)) for s in range(slots)}
 
         def serve_phase(r0, r1):
             for r in range(r0, r1):
@@ -573,7 +583,7 @@ def run_star(args):
                         while h.poll(timeout_us=120_000_000) is None:
                             raise RuntimeError("star verifier: send not done within 120 s")
                     L, tok = outs[s]
-                    h.serve(s, r, B, ppool[pidx(r, s)], L, tok, request_id_base=rid(rank, s))
+                    h.serve(s, r, Bv[rank], ppool[pidx(r, s)], L, tok, request_id_base=rid(rank, s))
             for _ in range(slots):
                 if h.poll(timeout_us=120_000_000) is None:
                     raise RuntimeError("star verifier: send not done within 120 s")
@@ -601,8 +611,9 @@ def run_star(args):
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": f"{args.config}: {c['name']}, star 1 -> {nver}"
                                    + (" (loopback on one GPU)" if loop else ""),
-                       "vocab": V, "k": k, "batch_per_verifier": B, "temperature": T,
-                       "kappa": c["kappa"], "logits": args.dtype, "slots": slots,
+                       "vocab": V, "k": k, "batch_per_verifier": [Bv[v] for v in range(1, nver + 1)],
+                       "temperature": T, "kappa": [Kv[v] for v in range(1, nver + 1)],
+                       "logits": args.dtype, "slots": slots,
                        "payload": args.payload,
                        "draft_standin": f"{k} x bf16 GEMM [{B},{args.draft_hidden}]x[{args.draft_hidden},{V}]"
                                         " + sd_draft_sample per verifier-round",
