@@ -61,6 +61,11 @@ def parse():
                     help="star: per-verifier batch sizes, comma-separated (C4 heterogeneous star)")
     ap.add_argument("--kappas", default="",
                     help="star: per-verifier draft/target agreement kappa, comma-separated (C4)")
+    ap.add_argument("--trace-seconds", type=float, default=0.0,
+                    help="star loopback: drive the verifiers' cohorts by a seeded bursty arrival "
+                         "trace for this many seconds (BASELINE C5)")
+    ap.add_argument("--burst-rate", type=float, default=20.0, help="C5: bursts per second per verifier")
+    ap.add_argument("--burst-mean", type=float, default=16.0, help="C5: mean requests per burst")
     return ap.parse_args()
 
 
@@ -645,8 +650,138 @@ def run_star(args):
         dist.destroy_process_group()
 
 
+def run_star_trace(args):
+    """BASELINE config 5 on one GPU (loopback star, N virtual verifiers): requests arrive by a
+    seeded compound-Poisson trace (workload.bursty_trace: bursts at --burst-rate per second per
+    verifier, Geometric(--burst-mean) requests per burst, 64..512 tokens each).  Each verifier
+    keeps --slots cohorts of up to B requests; a cohort with active requests issues its next round
+    when its previous one returned (closed loop), the draft serving rounds FIFO from Q_in
+    (Alg. 1); a round's batch is the cohort's current size; each request emits L+1 tokens per
+    round until its length is reached.  Reports the draft busy fraction overall and per 100 ms
+    window, per-verifier tokens/s and completed requests."""
+    import numpy as np
+    import torch
+
+    import paper_2601_21622_b200 as sd
+    from paper_2601_21622_b200 import star
+    from workload import make_batch_torch
+    from workload.trace import bursty_trace
+
+    nver = args.star_loopback
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    c = workload(args)
+    V, k, B, T = c["V"], c["k"], c["B"], c["T"]
+    slots = args.slots
+    tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
+    h = star.Star(0, nver + 1, B, k, V, T, seed=21622, n_slots=slots, dtype=tdt, device=dev,
+                  transport="loopback", timeout_ms=120000, payload=args.payload)
+    pool = {v: make_batch_torch(V, k, B, T, c["kappa"] or 30.0, c["seed"] + 7919 * v, dev,
+                                dtype=args.dtype) for v in range(1, nver + 1)}
+    Wt = torch.randn(args.draft_hidden, V, device=dev, dtype=torch.bfloat16) * 0.02
+    hid = torch.randn(B, args.draft_hidden, device=dev, dtype=torch.bfloat16)
+    bufs = {(v, s_): (torch.empty(B, dtype=torch.int32, device=dev),
+                      torch.empty(B, k + 1, dtype=torch.int32, device=dev))
+            for v in range(1, nver + 1) for s_ in range(slots)}
+    trace = bursty_trace(nver, args.trace_seconds, burst_rate_hz=args.burst_rate,
+                         burst_mean=args.burst_mean)
+    nxt = {v: 0 for v in trace}
+    pending = {v: [] for v in trace}                                 # arrived, not yet in a cohort
+    cohort = {(v, s_): [] for v in trace for s_ in range(slots)}     # [remaining tokens]
+    inflight = {(v, s_): None for v in trace for s_ in range(slots)}
+    rnd = {(v, s_): 0 for v in trace for s_ in range(slots)}
+    tokens = np.zeros(nver + 1)
+    done = np.zeros(nver + 1, dtype=np.int64)
+    win_tok = {}
+    keep = {}
+
+    def submit(v, s_, now):
+        n = len(cohort[(v, s_)])
+        q = pool[v]["q"][:n]
+        h.draft_begin(verifier=v)
+        for _ in range(k):                                                 # S(d) = d t_s
+            torch.matmul(hid[:n], Wt)
+        r = rnd[(v, s_)]
+        ids, qm, _ = sd.draft_sample(q, T, seed=21622, round=r, request_id_base=(v << 32) + s_ * B,
+                                     want_qmeta=args.payload == "qmeta")
+        h.draft_end()
+        L, tok = bufs[(v, s_)]
+        keep[(v, s_)] = (ids, qm)
+        h.submit(v, s_, r, ids, q, L[:n], tok[:n], request_id_base=(v << 32) + s_ * B,
+                 p=pool[v]["p"][:n], qmeta=qm)
+        inflight[(v, s_)] = n
+        rnd[(v, s_)] = r + 1
+
+    t0 = time.perf_counter()
+    now_ms = lambda: (time.perf_counter() - t0) * 1000.0                  # noqa: E731
+    end_ms = args.trace_seconds * 1000.0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    with ClockSampler(0) as clk:
+        while True:
+            t = now_ms()
+            if t < end_ms:
+                for v in trace:                                           # arrivals wait ...
+                    while nxt[v] < len(trace[v]) and trace[v][nxt[v]][0] <= t:
+                        pending[v].append(trace[v][nxt[v]][1])
+                        nxt[v] += 1
+                for (v, s_), n in inflight.items():                       # ... for an idle cohort
+                    if n is None:
+                        room = B - len(cohort[(v, s_)])
+                        cohort[(v, s_)] += pending[v][:room]
+                        del pending[v][:room]
+                        if cohort[(v, s_)]:
+                            submit(v, s_, t)
+            elif all(n is None for n in inflight.values()):
+                break
+            got = h.poll(timeout_us=200)
+            while got is not None:
+                v, s_, r = got
+                n = inflight[(v, s_)]
+                Lh = bufs[(v, s_)][0][:n].cpu().numpy()
+                rem = cohort[(v, s_)]
+                emit = np.minimum(Lh + 1, np.asarray(rem))
+                tokens[v] += emit.sum()
+                w = int(now_ms() // 100)
+                win_tok[w] = win_tok.get(w, 0) + int(emit.sum())
+                rem = [x - e for x, e in zip(rem, emit) if x - e > 0]
+                done[v] += n - len(rem)
+                cohort[(v, s_)] = rem
+                inflight[(v, s_)] = None
+                got = h.poll(timeout_us=0)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    st = h.stats()
+    line = {
+        "metric": METRIC, "value": float(tokens.sum()) / (ms / 1000.0), "unit": UNIT, "n_gpus": 1,
+        "steps": int(sum(rnd.values())), "warmup": 0, "ms_per_step": ms / max(1, sum(rnd.values())),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic",
+        "config": {"workload": f"c5: bursty arrival trace, star 1 -> {nver} (loopback on one GPU)",
+                   "vocab": V, "k": k, "max_batch_per_cohort": B, "slots": slots,
+                   "temperature": T, "kappa": c["kappa"], "payload": args.payload,
+                   "trace": {"seconds": args.trace_seconds, "burst_rate_hz": args.burst_rate,
+                             "burst_mean": args.burst_mean, "tokens_per_request": "64..512",
+                             "requests": int(sum(len(x) for x in trace.values()))}},
+        "star": {"busy_fraction": st["busy_fraction"], "mean_wait_ms": st["mean_wait_ms"],
+                 "rounds": st["rounds"],
+                 "per_verifier_tokens_s": (tokens[1:] / (ms / 1000.0)).tolist(),
+                 "completed_requests": done[1:].tolist(),
+                 "tokens_per_100ms": [win_tok.get(i, 0) for i in range(int(ms // 100) + 1)]},
+        "roofline": None, "e2e": None,
+        "gpu_launches": int(sum(rnd.values())) * (4 + (1 if args.payload == "qmeta" else 0)),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    h.close()
+
+
 def main():
     args = parse()
+    if args.star_loopback > 0 and args.trace_seconds > 0:
+        run_star_trace(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
