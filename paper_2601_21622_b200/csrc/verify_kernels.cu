@@ -1281,10 +1281,13 @@ __global__ void __launch_bounds__(kThreads, rs_min_blocks(GREEDY, sizeof(E))) k_
     // a group of gridDim.y requests all position-0 rows come first (position-major), then
     // position 1, ...; one group (gridDim.y = B) is the plain position-major order
     const int c = blockIdx.x;
-    const int grp = blockIdx.z / (kk + 1);
-    const int j = blockIdx.z - grp * (kk + 1);
-    const int b = grp * gridDim.y + blockIdx.y;
-    if (b >= P.B) return;
+    int b = blockIdx.y, j = blockIdx.z;
+    if (gridDim.z != static_cast<unsigned>(kk + 1)) {   // (more than one group: STARSD_RGROUP / B > 32768)
+        const int grp = j / (kk + 1);
+        j -= grp * (kk + 1);
+        b += grp * gridDim.y;
+        if (b >= P.B) return;
+    }
     const size_t pos = static_cast<size_t>(b) * (kk + 1) + j;
 
     const int rank = CL > 1 ? c % CL : 0;
