@@ -1318,7 +1318,6 @@ __global__ void __launch_bounds__(kThreads, rs_min_blocks(GREEDY, sizeof(E))) k_
             }
         }
         s_L = tL;
-        if (TAG) s_tag = (ld_relaxed_u32(P.epoch) + 1u) | 0x80000000u;
         s_flag = skip;
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -1377,9 +1376,12 @@ __global__ void __launch_bounds__(kThreads, rs_min_blocks(GREEDY, sizeof(E))) k_
     if (tid == 0) {
         mbar_arrive_expect_tx(&bar[0], bulk);
         if (bulk) bulk_g2s(sp, gp, bulk, &bar[0]);
-        // start ticket (tagged rows): its result is consumed at publish time, so the round trip
-        // overlaps the load and the statistics
-        if (TAG) tk = ticket_relaxed(P.ticketA + pos);
+        // start ticket and call tag (tagged rows): both are consumed at publish time (s_tag after
+        // the block reduction's barrier), so their round trips overlap the load and the statistics
+        if (TAG) {
+            tk = ticket_relaxed(P.ticketA + pos);
+            s_tag = (ld_relaxed_u32(P.epoch) + 1u) | 0x80000000u;
+        }
     } else if (tid == 32 && load_q) {
         mbar_arrive_expect_tx(&bar[1], bulk);
         if (bulk) bulk_g2s(sq, gq, bulk, &bar[1]);
