@@ -388,6 +388,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         E = args.e2e_steps
         etok = 0
+        zc_bytes = 0.0
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record()
@@ -397,15 +398,30 @@ def run_ours(args):
                                        seed=21622, round=i, request_id_base=rid0, device=dev,
                                        staging=staging)
             etok += int((Lo + 1)[(so & 7) == 0].sum())
+            Ln = Lo.numpy()
+            # zero copy: the rows the lazy path reads in place + the sampler's stop
+            # row pair (p_L, q_L) or bonus row p_k -- a lower bound: ncu shows ~1.1x (rows of the
+            # next position that load before a stop lands)
+            zc_bytes += float(algorithmic_bytes(Ln, V, k, e, greedy).sum())
+            if not greedy:
+                zc_bytes += float(((Ln < k) + 1).sum()) * V * e
         s1.record()
         torch.cuda.synchronize()
         ems = s0.elapsed_time(s1)
         (ems,), (etok_all,) = reduce_max_sum([ems], [etok], dev)
-        h2d = sum(hb[0][x].numel() * hb[0][x].element_size() for x in ("p", "q", "ids")
-                  if hb[0][x] is not None and not (greedy and x == "q"))   # q is not copied at T = 0
+        zero_copy = staging.get("p") is None                         # (verify_host's zero-copy path)
+        if zero_copy:
+            h2d = int(zc_bytes / E) + hb[0]["ids"].numel() * 4
+        else:
+            h2d = sum(hb[0][x].numel() * hb[0][x].element_size() for x in ("p", "q", "ids")
+                      if hb[0][x] is not None and not (greedy and x == "q"))   # no q at T = 0
         d2h = B * 4 + B * (k + 1) * 4 + B * 4
         e2e = {"value": etok_all / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": E}
+               "d2h_bytes_per_step": d2h, "steps": E,
+               "h2d_mode": ("zero copy: the kernels read the pinned host logits in place over PCIe "
+                            "(only the rows the lazy path needs); bytes = those rows + the "
+                            "sampler's stop rows, a lower bound" if zero_copy else
+                            "pinned host -> device copies of p, q, ids")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -92,8 +92,12 @@ typedef struct {
  * ties), t = argmax p_logits[b][L]; q_logits is not read and may be NULL (C-5).
  *
  * Arguments
- *   p_logits      device, [B][k+1][ld_p] elements of shape->dtype, rows 16-byte aligned
- *   q_logits      device, [B][k][ld_q], rows 16-byte aligned; may be NULL iff temperature == 0
+ *   p_logits      device, [B][k+1][ld_p] elements of shape->dtype, rows 16-byte aligned; or
+ *                 pinned host memory mapped into the device's address space (cudaHostAlloc /
+ *                 cudaHostRegister under unified addressing): the kernels then read it in place
+ *                 over PCIe, and the lazy path moves only the rows it needs (zero copy)
+ *   q_logits      device (or mapped pinned host), [B][k][ld_q], rows 16-byte aligned; may be NULL
+ *                 iff temperature == 0
  *   draft_ids     device, [B][k] int32
  *   shape         host pointer, read during the call only
  *   temperature   0 (greedy) or finite and >= 1e-3 (else SD_ERR_INVALID_ARGUMENT)

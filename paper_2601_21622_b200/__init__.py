@@ -305,17 +305,22 @@ def tree_verify(p: torch.Tensor, q: torch.Tensor | None, tree_tokens: torch.Tens
 
 def verify_host(p: torch.Tensor, q: torch.Tensor | None, ids: torch.Tensor, temperature: float,
                 seed: int = 0, round: int = 0, request_id_base: int = 0,
-                device: torch.device | str = "cuda", staging: dict | None = None):
-    """End-to-end call on HOST tensors (pinned for async copies): host->device copies of the
-    inputs, sd_verify, device->host copy of the results, then a stream synchronize.
-    `staging` (optional dict) caches the device buffers between calls."""
+                device: torch.device | str = "cuda", staging: dict | None = None,
+                zero_copy: bool = True):
+    """End-to-end call on HOST tensors.  Pinned logits (zero_copy, the default) are read by the
+    kernels in place: pinned memory is mapped into the device's address space, so sd_verify's bulk
+    copies pull over PCIe only the rows the lazy path needs (include/starsd.h).  Otherwise (or
+    unpinned logits) the logits are copied to the device first.  The draft ids go to the device,
+    the results come back, then a stream synchronize.  `staging` (optional dict) caches the device
+    buffers between calls."""
     dev = torch.device(device)
     st = staging if staging is not None else {}
-    sig = (tuple(p.shape), p.dtype, None if q is None else (tuple(q.shape), q.dtype), tuple(ids.shape))
+    zc = zero_copy and p.is_pinned() and (q is None or q.is_pinned())
+    sig = (tuple(p.shape), p.dtype, None if q is None else (tuple(q.shape), q.dtype), tuple(ids.shape), zc)
     if st.get("sig") != sig:
         st["sig"] = sig
-        st["p"] = torch.empty(p.shape, dtype=p.dtype, device=dev)
-        st["q"] = torch.empty(q.shape, dtype=q.dtype, device=dev) if q is not None else None
+        st["p"] = None if zc else torch.empty(p.shape, dtype=p.dtype, device=dev)
+        st["q"] = torch.empty(q.shape, dtype=q.dtype, device=dev) if q is not None and not zc else None
         st["ids"] = torch.empty(ids.shape, dtype=torch.int32, device=dev)
         B, k = ids.shape
         st["out"] = (torch.empty(B, dtype=torch.int32, device=dev),
@@ -323,16 +328,40 @@ def verify_host(p: torch.Tensor, q: torch.Tensor | None, ids: torch.Tensor, temp
                      torch.empty(B, dtype=torch.int32, device=dev))
         st["host_out"] = tuple(torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
                                for t in st["out"])
-    st["p"].copy_(p, non_blocking=True)
-    if q is not None:
-        st["q"].copy_(q, non_blocking=True)
     st["ids"].copy_(ids, non_blocking=True)
-    verify(st["p"], st["q"], st["ids"], temperature, seed, round, request_id_base,
-           out=st["out"])
+    if zc:
+        _verify_ptrs(p, q, st["ids"], temperature, seed, round, request_id_base, st["out"], dev)
+    else:
+        st["p"].copy_(p, non_blocking=True)
+        if q is not None:
+            st["q"].copy_(q, non_blocking=True)
+        verify(st["p"], st["q"], st["ids"], temperature, seed, round, request_id_base,
+               out=st["out"])
     for h, d in zip(st["host_out"], st["out"]):
         h.copy_(d, non_blocking=True)
     torch.cuda.current_stream(dev).synchronize()
     return st["host_out"]
+
+
+def _verify_ptrs(p, q, ids, temperature, seed, round, request_id_base, out, dev):
+    """sd_verify on pinned host logits (zero copy): the same marshalling as verify()."""
+    B, k1, ld_p = p.shape
+    k = k1 - 1
+    if p.stride(-1) != 1 or p.stride(-2) != ld_p or p.stride(0) != k1 * ld_p:
+        raise StarsdError("p must be contiguous [B, k+1, ld]")
+    ld_q = q.shape[-1] if q is not None else 0
+    if q is not None and (q.stride(-1) != 1 or q.stride(-2) != ld_q or q.stride(0) != k * ld_q):
+        raise StarsdError("q must be contiguous [B, k, ld]")
+    s = torch.cuda.current_stream(dev)
+    ws = _workspace_for(dev, s, B, k, ld_p, float(temperature), p.dtype)
+    sh = _shape(B, k, ld_p, ld_p, ld_q, _dtype_code(p))
+    L, tok, status = out
+    check(_lib.load().sd_verify(p.data_ptr(), q.data_ptr() if q is not None else None,
+                                ids.data_ptr(), ctypes.byref(sh), float(temperature),
+                                seed & (2**64 - 1), round & (2**64 - 1),
+                                request_id_base & (2**64 - 1), L.data_ptr(), tok.data_ptr(),
+                                status.data_ptr(), ws.buf.data_ptr(), ws.nbytes, s.cuda_stream),
+          "sd_verify (zero copy)")
 
 
 def verify_trace(p: torch.Tensor, accept_len: torch.Tensor, temperature: float,

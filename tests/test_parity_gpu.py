@@ -374,3 +374,24 @@ def test_one_workspace_serves_shapes_of_different_layout():
                             trace=True, n_threads=8)
         stats = compare(d, (L.cpu().numpy(), tok.cpu().numpy(), st.cpu().numpy()), ref, T, 4, i, 0)
         assert stats["ties"] <= max(1, 2e-2 * stats["n"]), stats
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_verify_host_zero_copy_and_copy_paths_match_the_device_call(dtype):
+    """verify_host: pinned host logits are read in place by the kernels (zero copy), unpinned ones
+    are copied first; both must equal the device-resident call bit for bit, sampled and greedy,
+    and one staging dict must survive switching between them (and between T = 0 and T > 0)."""
+    d = make_batch_torch(V=128256, k=7, B=24, T=1.0, kappa=30.0, seed=77, device=DEV, dtype=dtype)
+    staging = {}
+    for T in (1.0, 0.0, 1.0):
+        q = d["q"] if T > 0 else None
+        ref = [t.cpu() for t in sd.verify(d["p"], q, d["ids"], T, seed=5, round=2, request_id_base=9)]
+        torch.cuda.synchronize()
+        for pinned in (True, False):
+            hp = d["p"].cpu().pin_memory() if pinned else d["p"].cpu()
+            hq = None if q is None else (q.cpu().pin_memory() if pinned else q.cpu())
+            got = sd.verify_host(hp, hq, d["ids"].cpu(), T, seed=5, round=2, request_id_base=9,
+                                 staging=staging)
+            assert (staging["p"] is None) == pinned                      # the path taken
+            for a, b in zip(got, ref):
+                assert torch.equal(a, b), (dtype, T, pinned)
