@@ -403,7 +403,7 @@ def run_ours(args):
             # row pair (p_L, q_L) or bonus row p_k -- a lower bound: ncu shows ~1.1x (rows of the
             # next position that load before a stop lands)
             zc_bytes += float(algorithmic_bytes(Ln, V, k, e, greedy).sum())
-            if not greedy:
+            if not greedy and staging.get("p_stage") is None:
                 zc_bytes += float(((Ln < k) + 1).sum()) * V * e
         s1.record()
         torch.cuda.synchronize()
@@ -419,8 +419,9 @@ def run_ours(args):
         e2e = {"value": etok_all / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": E,
                "h2d_mode": ("zero copy: the kernels read the pinned host logits in place over PCIe "
-                            "(only the rows the lazy path needs); bytes = those rows + the "
-                            "sampler's stop rows, a lower bound" if zero_copy else
+                            "(only the rows the lazy path needs, each once: the sampler reads its "
+                            "stop rows from a device stage, sd_verify_staged); bytes = those rows, "
+                            "a lower bound" if zero_copy else
                             "pinned host -> device copies of p, q, ids")}
 
     cpu = None

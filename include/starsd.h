@@ -127,6 +127,24 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
                     int32_t* out_accept_len, int32_t* out_tokens, int32_t* out_status,
                     void* workspace, size_t workspace_bytes, cudaStream_t stream);
 
+/*
+ * sd_verify_staged -- sd_verify for logits that live in mapped pinned HOST memory (zero copy,
+ * see p_logits above): the statistics pass reads each row it needs over PCIe once and also writes
+ * it to a device stage; the sampling pass then reads its stop row (p_L, q_L -- or p_k) from the
+ * stage instead of crossing PCIe a second time.  Same arguments and results as sd_verify, plus
+ *   p_stage, q_stage  device, [B][k+1][ld_p] and [B][k][ld_q] elements of shape->dtype, 16-byte
+ *                     aligned, caller-owned; only the rows the call reads are written (contents
+ *                     are scratch).  Ignored at T = 0 (greedy has no sampling pass).
+ * The sampler then starts after the statistics kernel completes (no early launch).  Returns
+ * SD_ERR_INVALID_ARGUMENT for a NULL / misaligned stage at T > 0.
+ */
+sd_status sd_verify_staged(const void* p_logits, const void* q_logits, const int32_t* draft_ids,
+                           const sd_shape* shape, float temperature, uint64_t seed,
+                           uint64_t round, uint64_t request_id_base,
+                           int32_t* out_accept_len, int32_t* out_tokens, int32_t* out_status,
+                           void* workspace, size_t workspace_bytes, void* p_stage, void* q_stage,
+                           cudaStream_t stream);
+
 /* Bytes of workspace sd_verify needs for this shape/temperature (host only, no GPU work). */
 sd_status sd_verify_workspace_size(const sd_shape* shape, float temperature, size_t* bytes);
 

@@ -321,6 +321,10 @@ def verify_host(p: torch.Tensor, q: torch.Tensor | None, ids: torch.Tensor, temp
         st["sig"] = sig
         st["p"] = None if zc else torch.empty(p.shape, dtype=p.dtype, device=dev)
         st["q"] = torch.empty(q.shape, dtype=q.dtype, device=dev) if q is not None and not zc else None
+        # zero copy, sampled: device stages the statistics pass fills with the rows it reads, so
+        # the sampler's stop rows do not cross PCIe twice (sd_verify_staged)
+        st["p_stage"] = torch.empty(p.shape, dtype=p.dtype, device=dev) if zc and q is not None else None
+        st["q_stage"] = torch.empty(q.shape, dtype=q.dtype, device=dev) if zc and q is not None else None
         st["ids"] = torch.empty(ids.shape, dtype=torch.int32, device=dev)
         B, k = ids.shape
         st["out"] = (torch.empty(B, dtype=torch.int32, device=dev),
@@ -330,7 +334,8 @@ def verify_host(p: torch.Tensor, q: torch.Tensor | None, ids: torch.Tensor, temp
                                for t in st["out"])
     st["ids"].copy_(ids, non_blocking=True)
     if zc:
-        _verify_ptrs(p, q, st["ids"], temperature, seed, round, request_id_base, st["out"], dev)
+        _verify_ptrs(p, q, st["ids"], temperature, seed, round, request_id_base, st["out"], dev,
+                     st["p_stage"], st["q_stage"])
     else:
         st["p"].copy_(p, non_blocking=True)
         if q is not None:
@@ -343,8 +348,10 @@ def verify_host(p: torch.Tensor, q: torch.Tensor | None, ids: torch.Tensor, temp
     return st["host_out"]
 
 
-def _verify_ptrs(p, q, ids, temperature, seed, round, request_id_base, out, dev):
-    """sd_verify on pinned host logits (zero copy): the same marshalling as verify()."""
+def _verify_ptrs(p, q, ids, temperature, seed, round, request_id_base, out, dev, p_stage=None,
+                 q_stage=None):
+    """sd_verify / sd_verify_staged on pinned host logits (zero copy): the same marshalling as
+    verify()."""
     B, k1, ld_p = p.shape
     k = k1 - 1
     if p.stride(-1) != 1 or p.stride(-2) != ld_p or p.stride(0) != k1 * ld_p:
@@ -356,12 +363,15 @@ def _verify_ptrs(p, q, ids, temperature, seed, round, request_id_base, out, dev)
     ws = _workspace_for(dev, s, B, k, ld_p, float(temperature), p.dtype)
     sh = _shape(B, k, ld_p, ld_p, ld_q, _dtype_code(p))
     L, tok, status = out
-    check(_lib.load().sd_verify(p.data_ptr(), q.data_ptr() if q is not None else None,
-                                ids.data_ptr(), ctypes.byref(sh), float(temperature),
-                                seed & (2**64 - 1), round & (2**64 - 1),
-                                request_id_base & (2**64 - 1), L.data_ptr(), tok.data_ptr(),
-                                status.data_ptr(), ws.buf.data_ptr(), ws.nbytes, s.cuda_stream),
-          "sd_verify (zero copy)")
+    args = (p.data_ptr(), q.data_ptr() if q is not None else None, ids.data_ptr(), ctypes.byref(sh),
+            float(temperature), seed & (2**64 - 1), round & (2**64 - 1),
+            request_id_base & (2**64 - 1), L.data_ptr(), tok.data_ptr(), status.data_ptr(),
+            ws.buf.data_ptr(), ws.nbytes)
+    if p_stage is not None and temperature != 0.0:
+        check(_lib.load().sd_verify_staged(*args, p_stage.data_ptr(), q_stage.data_ptr(),
+                                           s.cuda_stream), "sd_verify_staged")
+    else:
+        check(_lib.load().sd_verify(*args, s.cuda_stream), "sd_verify (zero copy)")
 
 
 def verify_trace(p: torch.Tensor, accept_len: torch.Tensor, temperature: float,

@@ -27,7 +27,7 @@ EXPORTS = ["sd_verify", "sd_verify_workspace_size", "sd_philox_uniforms", "sd_st
            "sd_sched_create", "sd_sched_push", "sd_sched_pop", "sd_sched_service",
            "sd_sched_observe", "sd_sched_stats", "sd_sched_predict", "sd_sched_destroy",
            "sd_draft_workspace_size", "sd_draft_sample", "sd_draft_qmeta", "sd_verify_qmeta",
-           "sd_tree_verify"]
+           "sd_tree_verify", "sd_verify_staged"]
 
 
 class Shape(ctypes.Structure):
@@ -111,6 +111,9 @@ def load():
     L.sd_verify_qmeta.argtypes = [vp, vp, vp, vp, ctypes.POINTER(Shape), ctypes.c_float, u64, u64,
                                   u64, vp, vp, vp, vp, sz, vp]
     L.sd_verify_qmeta.restype = st
+    L.sd_verify_staged.argtypes = [vp, vp, vp, ctypes.POINTER(Shape), ctypes.c_float, u64, u64, u64,
+                                   vp, vp, vp, vp, sz, vp, vp, vp]
+    L.sd_verify_staged.restype = st
     L.sd_draft_workspace_size.argtypes = [ctypes.POINTER(Shape), ctypes.c_float, ctypes.POINTER(sz)]
     L.sd_draft_workspace_size.restype = st
     L.sd_draft_sample.argtypes = [vp, ctypes.POINTER(Shape), ctypes.c_float, u64, u64, u64, vp, vp,

@@ -208,7 +208,8 @@ static sd_status verify_impl(const void* p_logits, const void* q_logits, const Q
                              const int32_t* draft_ids, const sd_shape* shape, float temperature,
                              uint64_t seed, uint64_t round, uint64_t request_id_base,
                              int32_t* out_accept_len, int32_t* out_tokens, int32_t* out_status,
-                             void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+                             void* workspace, size_t workspace_bytes, cudaStream_t stream,
+                             void* p_stage = nullptr, void* q_stage = nullptr) {
     clear_error();
     int esz;
     sd_status s = check_shape(shape, temperature, &esz);
@@ -244,6 +245,15 @@ static sd_status verify_impl(const void* p_logits, const void* q_logits, const Q
     P.q = greedy ? nullptr : q_logits;
     P.qmeta = greedy ? nullptr : qmeta;
     P.ids = draft_ids;
+    if (!greedy && p_stage) {
+        // staged rows: the sampler reads them after k_row_stats is complete (no early launch,
+        // no in-kernel sampling, the grid form of k_row_stats)
+        P.p_stage = p_stage;
+        P.q_stage = q_stage;
+        P.early = 0;
+        P.fsample = 0;
+        P.pipe = 0;
+    }
     P.seed = seed;
     P.round = round;
     P.rid_base = request_id_base;
@@ -266,6 +276,21 @@ sd_status sd_verify(const void* p_logits, const void* q_logits, const int32_t* d
     return verify_impl(p_logits, q_logits, nullptr, draft_ids, shape, temperature, seed, round,
                        request_id_base, out_accept_len, out_tokens, out_status, workspace,
                        workspace_bytes, stream);
+}
+
+sd_status sd_verify_staged(const void* p_logits, const void* q_logits, const int32_t* draft_ids,
+                           const sd_shape* shape, float temperature, uint64_t seed, uint64_t round,
+                           uint64_t request_id_base, int32_t* out_accept_len, int32_t* out_tokens,
+                           int32_t* out_status, void* workspace, size_t workspace_bytes,
+                           void* p_stage, void* q_stage, cudaStream_t stream) {
+    if (temperature != 0.0f && (!p_stage || !q_stage || !aligned16(p_stage) || !aligned16(q_stage))) {
+        clear_error();
+        return fail(SD_ERR_INVALID_ARGUMENT, "p_stage / q_stage NULL or not 16-byte aligned (T > 0)");
+    }
+    return verify_impl(p_logits, q_logits, nullptr, draft_ids, shape, temperature, seed, round,
+                       request_id_base, out_accept_len, out_tokens, out_status, workspace,
+                       workspace_bytes, stream, temperature != 0.0f ? p_stage : nullptr,
+                       temperature != 0.0f ? q_stage : nullptr);
 }
 
 sd_status sd_verify_qmeta(const void* p_logits, const void* q_logits, const sd_qmeta* q_meta,

@@ -107,6 +107,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// ---- TMA 1-D bulk copy shared -> global (SASS: UBLKCP.G.S), bulk-group completion ---------------
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_addr(src)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// the shared-memory source of this thread's bulk stores has been read (it may be reused / freed)
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 // ---- math -----------------------------------------------------------------------------
 // 2^x on the SFU (MUFU.EX2); denormal results flush to 0.
 __device__ __forceinline__ float ex2_approx(float x) {

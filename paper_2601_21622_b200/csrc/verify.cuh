@@ -116,6 +116,8 @@ struct Params {
     int32_t fsample;
     unsigned long long* claimed; // [B] bits 0..62: chunk task c claimed; bit 63: outputs written
     int32_t early;               // k_sample_req launched during k_row_stats' last position wave
+    void* p_stage;               // sd_verify_staged: device copies of the rows k_row_stats reads
+    void* q_stage;               // (the sampling kernels then read their stop rows from here)
     int32_t pipe;                // k_row_pipe (pipelined persistent CTAs) instead of k_row_stats
     int32_t rgroup;              // k_row_stats grid: requests per group (grid order: group-major,
                                  // then position, request, chunk); B = one group (position-major)

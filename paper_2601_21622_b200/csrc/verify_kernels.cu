@@ -808,8 +808,8 @@ __device__ __forceinline__ bool sample_chunk(const Params& P, unsigned char* sme
     const bool use_q = L < kk;
     const float c2 = P.c2;
     const ResidParams rp = resid_params(rs, use_q);
-    const E* gp = static_cast<const E*>(P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
-    const E* gq = use_q ? static_cast<const E*>(P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q
+    const E* gp = static_cast<const E*>(P.p_stage ? P.p_stage : P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
+    const E* gq = use_q ? static_cast<const E*>(P.q_stage ? P.q_stage : P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q
                         : nullptr;
     const int c0 = c * P.CH;
     const int len = min(P.CH, P.V - c0);
@@ -884,8 +884,8 @@ __device__ __forceinline__ int32_t sample_search(const Params& P, int b, int L, 
     const bool use_q = L < kk;
     const float c2 = P.c2;
     const ResidParams rp = resid_params(rs, use_q);
-    const E* gp = static_cast<const E*>(P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
-    const E* gq = use_q ? static_cast<const E*>(P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q
+    const E* gp = static_cast<const E*>(P.p_stage ? P.p_stage : P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
+    const E* gq = use_q ? static_cast<const E*>(P.q_stage ? P.q_stage : P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q
                         : nullptr;
     __threadfence();
     // level 1: chunks, one lane each, warp scans over blocks of 32 chunks (carry between blocks)
@@ -1031,8 +1031,8 @@ __device__ __forceinline__ void fused_sample_task(const Params& P, unsigned char
     constexpr int SEGV = 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int kk = P.k, V = P.V, nch = P.nch;
-    const E* gp = static_cast<const E*>(P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
-    const E* gq = static_cast<const E*>(P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q;
+    const E* gp = static_cast<const E*>(P.p_stage ? P.p_stage : P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
+    const E* gq = static_cast<const E*>(P.q_stage ? P.q_stage : P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q;
     const int vpc = P.CH / VEC;                        // vectors per chunk (32 segments)
     const int nvv = (V + VEC - 1) / VEC;               // vectors of the row
     const int v0 = c * vpc;
@@ -1397,6 +1397,21 @@ __global__ void __launch_bounds__(kThreads, rs_min_blocks(GREEDY, sizeof(E))) k_
     const PartA pa0 = slice_partial<E, GREEDY>(P, sp, sq, c0, len, load_q, x, bar, 0u, 0u, s_d, s_s,
                                                 s_gi, s_f);
     if (tid == 0) SD_TR(P, 4);
+    if constexpr (!GREEDY) {
+        if (P.p_stage) {   // sd_verify_staged: this slice also goes to the device stage
+            E* dp = static_cast<E*>(P.p_stage) + static_cast<int64_t>(pos) * P.ld_p + c0;
+            E* dq = load_q ? static_cast<E*>(P.q_stage) + (static_cast<int64_t>(b) * kk + j) * P.ld_q + c0
+                           : nullptr;
+            if (bulk && (tid == 0 || (tid == 32 && load_q))) {
+                bulk_s2g(tid == 0 ? dp : dq, tid == 0 ? sp : sq, bulk);
+                bulk_wait_read();   // (the slice's shared memory may be released after this)
+            }
+            for (int i = static_cast<int>(bulk / sizeof(E)) + tid; i < len; i += kThreads) {
+                dp[i] = sp[i];
+                if (load_q) dq[i] = sq[i];
+            }
+        }
+    }
     if ((CL > 1 || TAG) && warp != 0) return;
     if (warp == 0) {
         PartA pa = pa0;
@@ -1984,8 +1999,8 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
     const bool hard = (rs.status & kHard) != 0;
     const bool use_q = L < kk;
     const float c2 = P.c2;
-    const E* gp = static_cast<const E*>(P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
-    const E* gq = use_q ? static_cast<const E*>(P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q
+    const E* gp = static_cast<const E*>(P.p_stage ? P.p_stage : P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
+    const E* gq = use_q ? static_cast<const E*>(P.q_stage ? P.q_stage : P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q
                         : nullptr;
     const int V = P.V;
     const int nvv = (V + VEC - 1) / VEC;                      // vectors of the row

@@ -147,3 +147,16 @@ def test_verify_plan_default_is_two_launch_with_16kb_chunks(lib):
     assert sd.plan(16, 3, 3000, 1.0)["cluster"] == 0           # one chunk per row
     with pytest.raises(sd.StarsdError):
         sd.plan(4, 40, 1000, 1.0)                               # k > 31 rejected on the host
+
+
+def test_verify_staged_rejects_missing_or_misaligned_stages_on_host(lib):
+    """sd_verify_staged validates its stage buffers before any GPU work (T > 0 needs both)."""
+    import ctypes
+    SD_ERR_INVALID_ARGUMENT = 1
+    sh = shape()
+    fake = ctypes.c_void_p(0x10000)
+    for ps, qs in ((None, None), (fake, None), (None, fake), (ctypes.c_void_p(0x10008), fake)):
+        rc = lib.sd_verify_staged(fake, fake, fake, ctypes.byref(sh), 1.0, 0, 0, 0, fake, fake, None,
+                                  fake, 1 << 20, ps, qs, None)
+        assert rc == SD_ERR_INVALID_ARGUMENT
+        assert b"stage" in lib.sd_last_error()
