@@ -61,6 +61,9 @@ def parse():
                     help="star: per-verifier batch sizes, comma-separated (C4 heterogeneous star)")
     ap.add_argument("--kappas", default="",
                     help="star: per-verifier draft/target agreement kappa, comma-separated (C4)")
+    ap.add_argument("--target-ms", type=float, default=0.0,
+                    help="star: the verifiers' target-model forward per round, as a device spin "
+                         "of this many ms before each verify (Z of Eq. 6; 0 = verify only)")
     ap.add_argument("--trace-seconds", type=float, default=0.0,
                     help="star loopback: drive the verifiers' cohorts by a seeded bursty arrival "
                          "trace for this many seconds (BASELINE C5)")
@@ -511,7 +514,7 @@ def run_star(args):
     ids_x = star.exchange_ids(rank, world) if not loop else None
     h = star.Star(0 if loop else rank, nver + 1, B, k, V, T, seed=21622, n_slots=slots, dtype=tdt,
                   device=dev, ids=ids_x, transport="loopback" if loop else "nccl",
-                  timeout_ms=120000, payload=args.payload)
+                  timeout_ms=120000, payload=args.payload, target_ms=args.target_ms)
     rid = lambda v, s: (v << 32) + s * B                                  # noqa: E731
     pidx = lambda r, s: (r + s) % npool                                    # noqa: E731
     total_rounds = W + K
@@ -636,7 +639,7 @@ def run_star(args):
                        "vocab": V, "k": k, "batch_per_verifier": [Bv[v] for v in range(1, nver + 1)],
                        "temperature": T, "kappa": [Kv[v] for v in range(1, nver + 1)],
                        "logits": args.dtype, "slots": slots,
-                       "payload": args.payload,
+                       "payload": args.payload, "target_ms": args.target_ms,
                        "draft_standin": f"{k} x bf16 GEMM [{B},{args.draft_hidden}]x[{args.draft_hidden},{V}]"
                                         " + sd_draft_sample per verifier-round",
                        "parallelism": f"star: rank 0 draft, {nver} verifiers"},
