@@ -63,6 +63,14 @@ __device__ __forceinline__ uint32_t cl_map(const void* p, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
     return r;
 }
+__device__ __forceinline__ double cl_ld_f64(uint32_t raddr) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(raddr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cl_sync() {   // full cluster barrier (release / acquire)
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
 __device__ __forceinline__ void cl_st_v4(uint32_t raddr, uint4 v) {
     asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(raddr), "r"(v.x),
                  "r"(v.y), "r"(v.z), "r"(v.w)

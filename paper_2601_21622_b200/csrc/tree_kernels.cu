@@ -22,6 +22,8 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <atomic>
+#include <cstdlib>
 
 #include "philox.cuh"
 #include "ptx.cuh"
@@ -401,8 +403,473 @@ __global__ void __launch_bounds__(kTT) k_tree_verify(const TreeParams P) {
     }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// k_tree_cluster: the same walk with one 8-CTA cluster per request.  CTA rank r keeps its slice
+// of the current node's p and q rows (vectors [r SV, (r+1) SV)) in shared memory -- one TMA load
+// per row per node, the algorithmic minimum -- and every pass of the node (statistics, the
+// residual masses of the rejected candidates, the inverse CDF) runs on chip; the cluster combines
+// the slices' partials through distributed shared memory (each CTA posts its partial, a cluster
+// barrier, every CTA reads all eight in rank order, so every CTA takes the same decisions).
+// Same readings and counters as k_tree_verify (D-2, C-8, C-9); sums fp64 above one vector.
+constexpr int kTCMax = 16;               // CTAs per cluster (one request): 8 or 16
+constexpr int kTCT = 256;                // threads per CTA
+constexpr int kTCW = kTCT / 32;
+constexpr int kTCMaxBytes = 200 * 1024;  // shared memory for the two slices
+
+struct TCSmem {
+    float redf[kTCW];
+    double redd[kTCW];
+    int redi[kTCW];
+    double scan[kTCT];
+    double post[2][4];                   // this CTA's partials, double-buffered by phase
+    int bc;
+};
+
+__device__ __forceinline__ float tc_max(float v, TCSmem& s) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = t_max_nan(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+    __syncthreads();
+    if (lane == 0) s.redf[w] = v;
+    __syncthreads();
+    float r = s.redf[0];
+    for (int i = 1; i < kTCW; ++i) r = t_max_nan(r, s.redf[i]);
+    return r;
+}
+__device__ __forceinline__ double tc_sum(double v, TCSmem& s) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    __syncthreads();
+    if (lane == 0) s.redd[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    for (int i = 0; i < kTCW; ++i) r += s.redd[i];
+    return r;
+}
+// every CTA posts K values; after the cluster barrier every thread holds all ranks' posts
+template <int kTC, int K>
+__device__ __forceinline__ void tc_exchange(TCSmem& s, int& ph, const double (&mine)[K],
+                                            double (&all)[kTC][K]) {
+    double* slot = s.post[ph & 1];
+    if (threadIdx.x == 0)
+        #pragma unroll
+        for (int i = 0; i < K; ++i) slot[i] = mine[i];
+    cl_sync();
+    #pragma unroll
+    for (int r = 0; r < kTC; ++r)
+        #pragma unroll
+        for (int i = 0; i < K; ++i) all[r][i] = cl_ld_f64(cl_map(slot + i, r));
+    ++ph;
+}
+
+template <typename E, int kTC>
+__global__ void __launch_bounds__(kTCT, kTC == 16 ? 2 : 1) k_tree_cluster(const TreeParams P) {
+    using TE = TElt<E>;
+    constexpr int VEC = TE::VEC;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ TCSmem s;
+    __shared__ __align__(8) uint64_t bar[2];
+    const int b = blockIdx.x / kTC;
+    const int rank = static_cast<int>(cl_rank());
+    const int m = P.m, d = P.d, V = P.V;
+    const bool greedy = P.c2 == 0.0f;
+    const uint64_t rid = P.rid_base + static_cast<uint64_t>(b);
+    const int32_t* tok = P.tok + static_cast<size_t>(b) * P.N;
+    const int nvv = (V + VEC - 1) / VEC;
+    const int SV = (nvv + kTC - 1) / kTC;                  // vectors per slice
+    const int v0 = rank * SV, nv = max(0, min(SV, nvv - v0));
+    const uint4* sp = reinterpret_cast<const uint4*>(smem);
+    const uint4* sq = sp + SV;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    int ph = 0;                                            // cluster exchange phase
+    uint32_t lp = 0;                                       // node loads (mbarrier parity)
+    int node = 0, depth = 0, status = 0, emitted = -1, writer = 0;
+    int32_t path[32];
+    auto elem = [&](const uint4* base, int g, float (&v)[VEC]) {
+        const uint4 u = base[g];
+        if constexpr (VEC == 4) {
+            v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y);
+            v[2] = __uint_as_float(u.z); v[3] = __uint_as_float(u.w);
+        } else {
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                v[2 * i] = __uint_as_float(w[i] << 16);
+                v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+            }
+        }
+    };
+    while (true) {
+        const bool internal = depth < d;
+        const char* prow = static_cast<const char*>(P.p) + (static_cast<size_t>(b) * P.N + node) * P.ld_p * sizeof(E);
+        const char* qrow = internal && !greedy
+                               ? static_cast<const char*>(P.q) + (static_cast<size_t>(b) * P.Nint + node) * P.ld_q * sizeof(E)
+                               : nullptr;
+        // ---- this node's slices into shared memory (the previous node's reads are done) ------
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive_expect_tx(&bar[0], nv * 16u);
+            if (nv) bulk_g2s(smem, prow + static_cast<size_t>(v0) * 16, nv * 16u, &bar[0]);
+        } else if (threadIdx.x == 32) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint32_t nb = qrow ? nv * 16u : 0u;
+            mbar_arrive_expect_tx(&bar[1], nb);
+            if (nb) bulk_g2s(smem + static_cast<size_t>(SV) * 16, qrow + static_cast<size_t>(v0) * 16, nb, &bar[1]);
+        }
+        mbar_wait(&bar[0], lp & 1u);
+        mbar_wait(&bar[1], lp & 1u);
+        ++lp;
+        if (greedy) {
+            // (max, lowest index) over the row; NaN / +inf faults
+            float v = -INFINITY, nanacc = -INFINITY;
+            int gi = INT_MAX;
+            for (int g = threadIdx.x; g < nv; g += kTCT) {
+                float x[VEC];
+                elem(sp, g, x);
+#pragma unroll
+                for (int e = 0; e < VEC; ++e)
+                    if ((v0 + g) * VEC + e < V) {
+                        nanacc = t_max_nan(nanacc, x[e]);
+                        if (x[e] > v) v = x[e], gi = (v0 + g) * VEC + e;
+                    }
+            }
+            nanacc = tc_max(nanacc, s);
+            // block argmax (value, lowest index)
+            {
+                const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float ov = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+                    const int oi = __shfl_xor_sync(0xFFFFFFFFu, gi, o);
+                    if (ov > v || (ov == v && oi < gi)) v = ov, gi = oi;
+                }
+                __syncthreads();
+                if (lane == 0) s.redf[w] = v, s.redi[w] = gi;
+                __syncthreads();
+                v = s.redf[0];
+                gi = s.redi[0];
+                for (int i = 1; i < kTCW; ++i)
+                    if (s.redf[i] > v || (s.redf[i] == v && s.redi[i] < gi)) v = s.redf[i], gi = s.redi[i];
+            }
+            double all[kTC][3];
+            const double mine[3] = {static_cast<double>(v), static_cast<double>(gi), static_cast<double>(nanacc)};
+            tc_exchange<kTC, 3>(s, ph, mine, all);
+            float V_ = -INFINITY, nan_ = -INFINITY;
+            int G_ = INT_MAX;
+            #pragma unroll
+            for (int r = 0; r < kTC; ++r) {
+                const float rv = static_cast<float>(all[r][0]);
+                const int ri = static_cast<int>(all[r][1]);
+                nan_ = t_max_nan(nan_, static_cast<float>(all[r][2]));
+                if (rv > V_ || (rv == V_ && ri < G_)) V_ = rv, G_ = ri;
+            }
+            if (!(nan_ < INFINITY)) { status = kNonfinite; break; }
+            if (!(V_ > -INFINITY)) { status = kEmptyRow; break; }
+            if (depth == d) { emitted = G_; break; }
+            int next = -1;
+            for (int i = 0; i < m; ++i) {
+                const int x = tok[m * node + 1 + i];
+                if (x < 0 || x >= V) { status = kBadId; break; }
+                if (x == G_) { next = m * node + 1 + i; break; }
+            }
+            if (status) break;
+            if (next < 0) { emitted = G_; break; }
+            path[depth++] = G_;
+            node = next;
+            continue;
+        }
+        // ---- statistics of p (and q): slice (max, sum), combined over the cluster -------------
+        float Dl[2] = {-INFINITY, -INFINITY};
+        double Sl[2] = {0.0, 0.0};
+        for (int w = 0; w < (qrow ? 2 : 1); ++w) {
+            const uint4* base = w ? sq : sp;
+            float mx = -INFINITY;
+            for (int g = threadIdx.x; g < nv; g += kTCT) {
+                float x[VEC];
+                elem(base, g, x);
+#pragma unroll
+                for (int e = 0; e < VEC; ++e)
+                    if ((v0 + g) * VEC + e < V) mx = t_max_nan(mx, x[e]);
+            }
+            mx = tc_max(mx, s);
+            const float D = mx * P.c2;
+            double acc = 0.0;
+            if (mx < INFINITY && mx > -INFINITY) {
+                for (int g = threadIdx.x; g < nv; g += kTCT) {
+                    float x[VEC];
+                    elem(base, g, x);
+                    float t = 0.0f;
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e)
+                        if ((v0 + g) * VEC + e < V) t += ex2_approx(__fmaf_rn(x[e], P.c2, -D));
+                    acc += t;
+                }
+            }
+            Dl[w] = !(mx < INFINITY) ? NAN : D;
+            Sl[w] = tc_sum(acc, s);
+        }
+        double all[kTC][4];
+        {
+            const double mine[4] = {static_cast<double>(Dl[0]), Sl[0], static_cast<double>(Dl[1]), Sl[1]};
+            tc_exchange<kTC, 4>(s, ph, mine, all);
+        }
+        NodeDist nd;
+        int fp = 0, fq = 0;
+        {
+            float Dp = -INFINITY, Dq = -INFINITY;
+            #pragma unroll
+            for (int r = 0; r < kTC; ++r) {
+                Dp = t_max_nan(Dp, static_cast<float>(all[r][0]));
+                Dq = t_max_nan(Dq, static_cast<float>(all[r][2]));
+            }
+            double Sp = 0.0, Sq = 0.0;
+            #pragma unroll
+            for (int r = 0; r < kTC; ++r) {
+                if (all[r][1] > 0.0) Sp += all[r][1] * exp2(all[r][0] - static_cast<double>(Dp));
+                if (all[r][3] > 0.0) Sq += all[r][3] * exp2(all[r][2] - static_cast<double>(Dq));
+            }
+            fp = !(Dp < INFINITY) ? kNonfinite : (!(Dp > -INFINITY) ? kEmptyRow : 0);
+            if (qrow) fq = !(Dq < INFINITY) ? kNonfinite : (!(Dq > -INFINITY) ? kEmptyRow : 0);
+            nd.Dp = Dp; nd.Sp = Sp; nd.ip = static_cast<float>(1.0 / Sp);
+            nd.Dq = Dq; nd.Sq = Sq; nd.iq = qrow ? static_cast<float>(1.0 / Sq) : 0.0f;
+        }
+        if (fp) { status = fp; break; }
+        // the slice's terms of level lv (raw last level), and the inverse CDF over the cluster
+        auto slice_mass = [&](int lv, bool use_q) -> double {
+            double acc = 0.0;
+            for (int g = threadIdx.x; g < nv; g += kTCT) {
+                float vp[VEC], vq[VEC];
+                elem(sp, g, vp);
+                if (use_q) elem(sq, g, vq);
+                float t = 0.0f;
+#pragma unroll
+                for (int e = 0; e < VEC; ++e)
+                    if ((v0 + g) * VEC + e < V) t += dlevel(vp[e], use_q ? vq[e] : 0.0f, P.c2, nd, lv, true);
+                acc += t;
+            }
+            return tc_sum(acc, s);
+        };
+        // Inverse CDF over the cluster: per-thread contiguous ranges of the slice, the slice
+        // total posted with the slice's last positive-mass token (one exchange), the owner rank
+        // found in rank order, and the owner CTA's owner thread walks its range.  Returns the
+        // total mass (every CTA); *owner_out = the writing rank, *tok_out = the token (valid in
+        // the writing CTA).
+        auto sample = [&](int lv, bool use_q, int* owner_out, int* tok_out) -> double {
+            const int W = (nv + kTCT - 1) / kTCT;
+            const int g0 = threadIdx.x * W, g1 = min(nv, g0 + W);
+            double mine = 0.0;
+            int lastpos = -1;
+            for (int g = g0; g < g1; ++g) {
+                float vp[VEC], vq[VEC];
+                elem(sp, g, vp);
+                if (use_q) elem(sq, g, vq);
+                float t = 0.0f;
+#pragma unroll
+                for (int e = 0; e < VEC; ++e)
+                    if ((v0 + g) * VEC + e < V) {
+                        const float x = dlevel(vp[e], use_q ? vq[e] : 0.0f, P.c2, nd, lv, true);
+                        t += x;
+                        if (x > 0.0f) lastpos = (v0 + g) * VEC + e;
+                    }
+                mine += t;
+            }
+            s.scan[threadIdx.x] = mine;
+            __syncthreads();
+            if (threadIdx.x == 0) {                        // sequential exclusive scan, fixed order
+                double run = 0.0;
+                for (int i = 0; i < kTCT; ++i) {
+                    const double v = s.scan[i];
+                    s.scan[i] = run;
+                    run += v;
+                }
+                s.redd[0] = run;
+                s.bc = -1;
+            }
+            __syncthreads();
+            const double tot_r = s.redd[0];
+            int lp2 = lastpos;                             // the slice's last positive-mass token
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) lp2 = max(lp2, __shfl_xor_sync(0xFFFFFFFFu, lp2, o));
+            if ((threadIdx.x & 31) == 0) atomicMax(&s.bc, lp2);
+            __syncthreads();
+            const int last_r = s.bc;
+            double allm[kTC][2];
+            const double post[2] = {tot_r, static_cast<double>(last_r)};
+            tc_exchange<kTC, 2>(s, ph, post, allm);
+            double total = 0.0;
+#pragma unroll
+            for (int r = 0; r < kTC; ++r) total += allm[r][0];
+            const double u = unit24(verify_words(P.seed, static_cast<uint32_t>(depth), P.round, rid).y);
+            const double theta = u * total;
+            int owner = -1, lastr = -1;
+            double before = 0.0, acc = 0.0;
+#pragma unroll
+            for (int r = 0; r < kTC; ++r) {
+                if (allm[r][0] > 0.0) lastr = r;
+                if (owner < 0 && allm[r][0] > 0.0 && theta >= acc && theta < acc + allm[r][0]) {
+                    owner = r;
+                    before = acc;
+                }
+                acc += allm[r][0];
+            }
+            if (owner < 0) {                               // rounding: the last token with mass
+                *owner_out = 0;
+                *tok_out = lastr >= 0 ? static_cast<int>(allm[lastr][1]) : 0;
+                return total;
+            }
+            *owner_out = owner;
+            *tok_out = -1;
+            if (owner == rank) {
+                __syncthreads();
+                if (threadIdx.x == 0) s.bc = -1;
+                __syncthreads();
+                const double lo = before + s.scan[threadIdx.x];
+                if (mine > 0.0 && theta >= lo && theta < lo + mine) {
+                    double run = lo;
+                    int found = -1;
+                    for (int g = g0; g < g1 && found < 0; ++g) {
+                        float vp[VEC], vq[VEC];
+                        elem(sp, g, vp);
+                        if (use_q) elem(sq, g, vq);
+                        float t = 0.0f;
+                        for (int e = 0; e < VEC && found < 0; ++e)
+                            if ((v0 + g) * VEC + e < V) {
+                                const float x = dlevel(vp[e], use_q ? vq[e] : 0.0f, P.c2, nd, lv, true);
+                                if (x > 0.0f && run + static_cast<double>(t + x) > theta) found = (v0 + g) * VEC + e;
+                                t += x;
+                            }
+                        run += t;
+                    }
+                    if (found < 0) found = lastpos;
+                    atomicMax(&s.bc, found);
+                }
+                __syncthreads();
+                *tok_out = s.bc >= 0 ? s.bc : last_r;
+            }
+            return total;
+        };
+        if (depth == d) {                                  // leaf: bonus t ~ p_leaf (C-3)
+            sample(0, false, &writer, &emitted);
+            break;
+        }
+        if (fq) { status = fq; break; }
+        int next = -1;
+        for (int i = 0; i < m && next < 0; ++i) {
+            const int x = tok[m * node + 1 + i];
+            if (x < 0 || x >= V) { status = kBadId; break; }
+            if (i > 0) {                                   // d_i = norm(max(0, d_{i-1} - q))
+                nd.iR[i] = 0.0f;                           // (raw level i: max(0, d_{i-1} - q))
+                const double loc = slice_mass(i, true);
+                double allr[kTC][1];
+                const double mine1[1] = {loc};
+                tc_exchange<kTC, 1>(s, ph, mine1, allr);
+                double R = 0.0;
+                #pragma unroll
+                for (int r = 0; r < kTC; ++r) R += allr[r][0];
+                nd.R[i] = R;
+                nd.iR[i] = R > 0.0 ? static_cast<float>(1.0 / R) : -1.0f;
+                if (!(R > 0.0)) status |= kZeroResidual;
+            }
+            const float zp = TE::one(prow, x), zq = TE::one(qrow, x);
+            const double dx = static_cast<double>(dlevel(zp, zq, P.c2, nd, i, false));
+            const double qx = static_cast<double>(ex2_approx(__fmaf_rn(zq, P.c2, -nd.Dq)) * nd.iq);
+            const double a = qx > 0.0 ? dx / qx : 0.0;
+            if (zq == -INFINITY) status |= kZeroQ;
+            if (!(a >= 1.0)) {
+                const double u = unit24(verify_words(P.seed, static_cast<uint32_t>(depth + 32 * i), P.round, rid).x);
+                if (u >= a) continue;
+            }
+            next = m * node + 1 + i;
+            path[depth] = x;
+        }
+        if (status & kHard) break;
+        if (next >= 0) {
+            ++depth;
+            node = next;
+            continue;
+        }
+        {                                                  // every candidate rejected: t ~ d_m
+            // the sampling exchange also yields R_m = max(0, d_{m-1} - q)'s total mass
+            nd.iR[m] = 0.0f;                               // (raw level m: max(0, d_{m-1} - q))
+            const double R = sample(m, true, &writer, &emitted);
+            nd.R[m] = R;
+            if (!(R > 0.0)) {                              // C-6: d_m = d_{m-1}
+                status |= kZeroResidual;
+                nd.iR[m] = -1.0f;
+                sample(m, true, &writer, &emitted);
+            }
+        }
+        break;
+    }
+    if (rank == writer && threadIdx.x == 0) {   // (the rank that holds the emitted token)
+        const bool hard = (status & kHard) != 0;
+        const int L = hard ? 0 : depth;
+        P.out_L[b] = L;
+        int32_t* ot = P.out_tok + static_cast<size_t>(b) * (d + 1);
+        for (int i = 0; i <= d; ++i) ot[i] = hard ? -1 : (i < L ? path[i] : (i == L ? emitted : -1));
+        if (P.out_status) P.out_status[b] = status;
+        if (P.out_node) P.out_node[b] = node;
+    }
+    cl_sync();   // (no CTA leaves while a peer may still read its posts)
+}
+
+template <typename E, int CT>
+static cudaError_t launch_tree_cluster(const TreeParams& P, size_t smem, cudaStream_t st) {
+    static std::atomic<uint64_t> optin{0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(optin.load(std::memory_order_acquire) & bit)) {
+        e = cudaFuncSetAttribute(k_tree_cluster<E, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kTCMaxBytes));
+        if (e != cudaSuccess) return e;
+        if (CT > 8) {
+            e = cudaFuncSetAttribute(k_tree_cluster<E, CT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+        }
+        optin.fetch_or(bit, std::memory_order_acq_rel);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(P.B) * CT);
+    cfg.blockDim = dim3(kTCT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CT;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_tree_cluster<E, CT>, P);
+}
+
 cudaError_t launch_tree(const TreeParams& P, bool bf16, cudaStream_t st) {
     if (P.B == 0) return cudaSuccess;
+    // one 8-CTA cluster per request when the node's two row slices fit in shared memory
+    // (V <= ~200K fp32 / ~400K bf16); else one CTA per request streaming the rows
+    // (STARSD_TREE_CLUSTER = 0: off; 8 (default) or 16 CTAs per cluster -- 16 measured slower)
+    static const int cl = getenv("STARSD_TREE_CLUSTER") ? atoi(getenv("STARSD_TREE_CLUSTER")) : 8;
+    const int VEC = bf16 ? 8 : 4;
+    const int CT = cl == 8 ? 8 : 16;
+    const size_t SV = ((P.V + VEC - 1) / VEC + CT - 1) / CT;
+    const size_t smem = 2 * SV * 16;
+    if (cl && smem <= static_cast<size_t>(kTCMaxBytes) && P.d <= 31) {
+        if (CT == 8)
+            return bf16 ? launch_tree_cluster<__nv_bfloat16, 8>(P, smem, st)
+                        : launch_tree_cluster<float, 8>(P, smem, st);
+        return bf16 ? launch_tree_cluster<__nv_bfloat16, 16>(P, smem, st)
+                    : launch_tree_cluster<float, 16>(P, smem, st);
+    }
     if (bf16) k_tree_verify<__nv_bfloat16><<<P.B, kTT, 0, st>>>(P);
     else k_tree_verify<float><<<P.B, kTT, 0, st>>>(P);
     return cudaGetLastError();
