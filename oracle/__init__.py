@@ -20,7 +20,6 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "starsd_ref.c")
 _LIB_PATH = os.path.join(_HERE, "libstarsd_ref.so")
 KMAX = 31
-NDRAW = 32          # C-15: rejection draws before the inverse-CDF fallback (starsd_ref.h)
 
 FAULT_BAD_DRAFT_ID = 1
 FAULT_NONFINITE = 2
@@ -52,9 +51,7 @@ class Trace(ctypes.Structure):
                 ("u_acc", ctypes.c_double * KMAX),
                 ("R", ctypes.c_double), ("u_smp", ctypes.c_double), ("theta", ctypes.c_double),
                 ("C_prev", ctypes.c_double), ("C_tok", ctypes.c_double),
-                ("mu_a", ctypes.c_double), ("mu_s", ctypes.c_double),
-                ("n_draw", ctypes.c_int32), ("reserved", ctypes.c_int32),
-                ("v_acc", ctypes.c_double), ("a_res", ctypes.c_double)]
+                ("mu_a", ctypes.c_double), ("mu_s", ctypes.c_double)]
 
 
 _lib = None
@@ -94,8 +91,6 @@ def lib():
         L.sd_ref_philox4x32_10.restype = None
         L.sd_ref_uniforms.argtypes = [u64, ctypes.c_uint32, u64, u64, vp, vp]
         L.sd_ref_uniforms.restype = None
-        L.sd_ref_draw_uniforms.argtypes = [u64, ctypes.c_uint32, ctypes.c_uint32, u64, u64, vp, vp]
-        L.sd_ref_draw_uniforms.restype = None
         _lib = L
     return _lib
 
@@ -285,10 +280,3 @@ def uniforms(seed, j, round, rid):
     ua, us = ctypes.c_double(), ctypes.c_double()
     lib().sd_ref_uniforms(seed, j, round, rid, ctypes.byref(ua), ctypes.byref(us))
     return ua.value, us.value
-
-
-def draw_uniforms(seed, L, n, round, rid):
-    """C-15: (theta_u, v) of rejection draw n at stop position L."""
-    tu, v = ctypes.c_double(), ctypes.c_double()
-    lib().sd_ref_draw_uniforms(seed, L, n, round, rid, ctypes.byref(tu), ctypes.byref(v))
-    return tu.value, v.value

@@ -22,11 +22,6 @@
  *   C-10 0-based: p rows j = 0..k, q rows j = 0..k-1; residual at L uses (p_L, q_L)
  *   C-11 fp64 throughout
  *   C-12 -inf logits allowed; NaN, +inf, an all -inf row, or a draft id outside [0,V) are faults
- *   C-15 the correction token t ~ norm(max(0, p_L - q_L)) is drawn by rejection from p_L:
- *        draws n = 0..NDRAW-1, candidate y_n = inverse CDF of p_L at theta_n (C-9 rule), accepted
- *        iff v_n < 1 - q_L(y_n)/p_L(y_n); the first accepted draw is t; if all NDRAW are rejected,
- *        t = the C-9 inverse CDF of the residual (theta = u_smp R) -- exact either way:
- *        Pr(t) = sum_n (1-R)^n r(t) + (1-R)^NDRAW r(t)/R = r(t)/R
  * It is lazy: rows after the first rejection are never read (the method's data dependency).
  */
 #include "starsd_ref.h"
@@ -73,17 +68,6 @@ void sd_ref_uniforms(uint64_t seed, uint32_t j, uint64_t round, uint64_t rid,
     sd_ref_philox4x32_10(ctr, key, w);
     if (u_acc) *u_acc = sd_ref_u24(w[0]);
     if (u_smp) *u_smp = sd_ref_u24(w[1]);
-}
-
-/* C-15: draw n's uniforms, counter (L + (n+1) 2^20, round, rid). */
-void sd_ref_draw_uniforms(uint64_t seed, uint32_t L, uint32_t n, uint64_t round, uint64_t rid,
-                          double* theta_u, double* v) {
-    uint32_t ctr[4] = {L + ((n + 1u) << 20), (uint32_t)round, (uint32_t)rid, (uint32_t)(rid >> 32)};
-    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
-    uint32_t w[4];
-    sd_ref_philox4x32_10(ctr, key, w);
-    if (theta_u) *theta_u = sd_ref_u24(w[0]);
-    if (v) *v = sd_ref_u24(w[1]);
 }
 
 /* ------------------------------------------------------------------------------------------
@@ -303,42 +287,13 @@ static void verify_sampled_one(const batch_t* a, int32_t b, double* buf) {
         emit(a, b, 0, -1, status);
         return;
     }
-    /* Correction (L < k) or bonus (L == k) (C-3, C-6, C-9, C-15). */
+    /* Correction (L < k) or bonus (L == k) (C-3, C-6, C-9). */
     int zero_res = 0;
     double R;
     row_t pr = p_row(a, b, L);
     if (L < k) {
         row_t qr = q_row(a, b, L);
-        /* C-15: rejection draws from p_L, accepted with probability 1 - q_L(y)/p_L(y) */
-        double Sp = 0.0;
-        for (int32_t y = 0; y < V; ++y) {
-            buf[y] = prob_of(pr, y, T, lam_p);
-            Sp += buf[y];
-        }
-        double mu = 1.0;
-        for (uint32_t n = 0; n < SD_REF_NDRAW; ++n) {
-            double tu, v, Cp, Ct;
-            sd_ref_draw_uniforms(a->seed, (uint32_t)L, n, a->round, rid, &tu, &v);
-            double theta = tu * Sp;
-            int32_t y = inverse_cdf(buf, V, theta, &Cp, &Ct);
-            double acc = 1.0 - prob_of(qr, y, T, lam_q) / buf[y];
-            double m1 = (theta - Cp) / Sp, m2 = (Ct - theta) / Sp, m3 = fabs(v - acc);
-            if (m1 < mu) mu = m1;
-            if (m2 < mu) mu = m2;
-            if (m3 < mu) mu = m3;
-            if (v < acc) {                                      /* accepted: t = y */
-                if (tr) {
-                    tr->L = L; tr->token = y; tr->status = status;
-                    tr->R = sampling_dist(pr, lam_p, &qr, lam_q, T, buf, &zero_res);
-                    tr->u_smp = tu; tr->theta = theta; tr->C_prev = Cp; tr->C_tok = Ct;
-                    tr->mu_s = mu; tr->n_draw = (int32_t)n + 1; tr->v_acc = v; tr->a_res = acc;
-                }
-                emit(a, b, L, y, status);
-                return;
-            }
-        }
-        if (tr) { tr->mu_s = mu; tr->n_draw = SD_REF_NDRAW + 1; }
-        R = sampling_dist(pr, lam_p, &qr, lam_q, T, buf, &zero_res);   /* fallback (C-9) */
+        R = sampling_dist(pr, lam_p, &qr, lam_q, T, buf, &zero_res);
     } else {
         int f = row_fault(pr);
         if (f) {
@@ -361,8 +316,7 @@ static void verify_sampled_one(const batch_t* a, int32_t b, double* buf) {
         tr->L = L; tr->token = t; tr->status = status;
         tr->R = R; tr->u_smp = u_smp; tr->theta = theta; tr->C_prev = Cp; tr->C_tok = Ct;
         double m1 = theta - Cp, m2 = Ct - theta;
-        double ms = (m1 < m2 ? m1 : m2) / R;
-        if (L == k || ms < tr->mu_s) tr->mu_s = ms;   /* (L < k: also the draws' margins) */
+        tr->mu_s = (m1 < m2 ? m1 : m2) / R;
     }
     emit(a, b, L, t, status);
 }
@@ -430,39 +384,7 @@ int sd_ref_sample_check(const void* p, const void* q, const int32_t* ids,
     double Rv;
     if (L < k) {
         row_t qr = q_row(&a, b, L);
-        double lam_q = row_logsumexp(qr, T);
-        /* C-15 draws: t is consistent as draw n's accepted candidate if theta_n lies in t's
-         * p-CDF cell within tau and v_n < a(t) + tau; a draw whose own candidate is accepted
-         * (or rejected) with margins >= tau decides (or passes) for every rounding */
-        const double tau = 1e-6;
-        double Sp = 0.0;
-        for (int32_t y = 0; y < V; ++y) {
-            buf[y] = prob_of(pr, y, T, lam_p);
-            Sp += buf[y];
-        }
-        double Cpt = 0.0;
-        for (int32_t y = 0; y < t; ++y) Cpt += buf[y];
-        double Ctt = Cpt + buf[t];
-        double at = buf[t] > 0.0 ? 1.0 - prob_of(qr, t, T, lam_q) / buf[t] : -1.0;
-        for (uint32_t n = 0; n < SD_REF_NDRAW; ++n) {
-            double tu, v, Cp, Ct;
-            sd_ref_draw_uniforms(seed, (uint32_t)L, n, round, rid_base + (uint64_t)b, &tu, &v);
-            double th = tu * Sp;
-            if (Cpt - tau * Sp <= th && th <= Ctt + tau * Sp && v < at + tau) {
-                *C_prev = Cpt; *C_tok = Ctt; *R = Sp; *theta = th;
-                free(buf);
-                return 0;
-            }
-            int32_t y = inverse_cdf(buf, V, th, &Cp, &Ct);
-            double acc = 1.0 - prob_of(qr, y, T, lam_q) / buf[y];
-            int robust = (th - Cp) >= tau * Sp && (Ct - th) >= tau * Sp && fabs(v - acc) >= tau;
-            if (robust && v < acc) {          /* the draw accepts another token for sure */
-                *C_prev = Cpt; *C_tok = Ctt; *R = Sp; *theta = th;
-                free(buf);
-                return 0;
-            }
-        }
-        Rv = sampling_dist(pr, lam_p, &qr, lam_q, T, buf, &zero_res);   /* fallback */
+        Rv = sampling_dist(pr, lam_p, &qr, row_logsumexp(qr, T), T, buf, &zero_res);
     } else {
         Rv = sampling_dist(pr, lam_p, NULL, 0.0, T, buf, &zero_res);
     }

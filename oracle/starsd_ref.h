@@ -46,22 +46,8 @@ typedef struct {
     double C_prev;        /* C(t-1): inclusive prefix mass before the emitted token       */
     double C_tok;         /* C(t)                                                         */
     double mu_a;          /* min_j |u_acc(j) - a_j| over tested j with ell<0 (1 if none)  */
-    double mu_s;          /* smallest sampling margin: over the evaluated rejection draws
-                             (C-15) the p-CDF cell margin / sum p and |v_n - a_n|; and, on the
-                             inverse-CDF path, min(theta - C(t-1), C(t) - theta) / R      */
-    int32_t n_draw;       /* C-15 draws evaluated: index of the accepted draw + 1; 0 at the
-                             bonus; SD_REF_NDRAW + 1 when every draw was rejected (fallback)  */
-    int32_t reserved;
-    double v_acc;         /* v of the accepted draw (0 if none)                           */
-    double a_res;         /* 1 - q_L(t)/p_L(t) of the accepted draw's candidate           */
+    double mu_s;          /* min(theta - C(t-1), C(t) - theta) / R                        */
 } sd_ref_trace;
-
-/* C-15: rejection draws of the correction token before the inverse-CDF fallback */
-#define SD_REF_NDRAW 32
-/* draw n's uniforms at stop position L: theta_u = u24(w0), v = u24(w1) of Philox counter
- * (L + (n + 1) * 2^20, round, rid) -- a counter domain disjoint from C-8's (j < 2^20) */
-void sd_ref_draw_uniforms(uint64_t seed, uint32_t L, uint32_t n, uint64_t round, uint64_t rid,
-                          double* theta_u, double* v);
 
 /* Philox4x32-10 (Salmon et al. 2011, Random123), restated. */
 void sd_ref_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);

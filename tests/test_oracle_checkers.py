@@ -34,48 +34,20 @@ def cell(cum, t):
     return (cum[t - 1] if t > 0 else 0.0), cum[t]
 
 
-def hand_draws(seed, L, round, rid, cum_p, acc):
-    """C-15 by hand: walk the rejection draws with the hand CDF of p_L and the hand table
-    acc[y] = 1 - q_L(y)/p_L(y); the candidate is numpy's searchsorted (first y with C(y) > theta),
-    the uniforms come from oracle.draw_uniforms (its counter layout is pinned below against a
-    direct Philox call).  Returns (token or None, draws evaluated, theta_u, v, smallest margin)."""
-    mu = 1.0
-    for n in range(oracle.NDRAW):
-        tu, v = oracle.draw_uniforms(seed, L, n, round, rid)
-        y = int(np.searchsorted(cum_p, tu, side="right"))
-        cp, ct = cell(cum_p, y)
-        mu = min(mu, tu - cp, ct - tu, abs(v - acc[y]))
-        if v < acc[y]:
-            return y, n + 1, tu, v, mu
-    return None, oracle.NDRAW + 1, None, None, mu
-
-
-def test_draw_uniforms_counter_layout():
-    """C-15: draw n at stop position L uses u24(w0), u24(w1) of Philox counter
-    (L + (n+1) 2^20, round, rid lo, rid hi) -- disjoint from C-8's counters (j < 2^20)."""
-    for (seed, L, n, rnd, rid) in [(42, 0, 0, 5, 7), (9, 3, 31, 2, (1 << 40) + 3), (2**40 + 1, 6, 5, 2**33 + 9, 0)]:
-        tu, v = oracle.draw_uniforms(seed, L, n, rnd, rid)
-        w = oracle.philox([L + ((n + 1) << 20), rnd & 0xFFFFFFFF, rid & 0xFFFFFFFF, rid >> 32],
-                          [seed & 0xFFFFFFFF, seed >> 32])
-        assert tu == (int(w[0]) >> 8) / 2.0 ** 24 and v == (int(w[1]) >> 8) / 2.0 ** 24
-
-
 # ---------------------------------------------------------------- trace fields -------------
 def test_trace_fields_on_the_inverse_cdf_hand_example():
     """Every trace field of the V=4 hand example: lam = 0 (logits are log-probs),
-    a_0 = 0.25, u_acc from Philox; at a rejection the C-15 draws (hand CDF of p_0, hand table
-    1 - q/p): token, draws evaluated, theta = theta_u (sum p = 1), the p-CDF cell, v, 1 - q/p,
-    R = 0.4 (the residual mass, reported for the tolerance tests) and mu_s = the smallest draw
-    margin; at acceptance the bonus CDF of p_1 with theta = u_smp; mu_a = |u - 0.25|."""
+    a_0 = 0.25, u_acc from Philox, and at a rejection R = 0.4, theta = 0.4 u_smp, the CDF cell of
+    the token from the hand residual [0, 0, .1, .3]; at acceptance the bonus CDF of p_1; mu_a =
+    |u - 0.25| and mu_s = min(theta - C(t-1), C(t) - theta) / R."""
     ex = WORKED["inverse_cdf_hand"]
     B = 2000
     p = np.broadcast_to(np.stack([logits(ex["p0"]), logits(ex["p1"])]), (B, 2, 4)).copy()
     q = np.broadcast_to(logits(ex["q0"])[None], (B, 1, 4)).copy()
     ids = np.zeros((B, 1), np.int32)
     L, tok, st, tr = oracle.verify(p, q, ids, 1.0, seed=42, round=5, rid_base=0, trace=True)
-    p_cum = np.cumsum(ex["p0"])
+    res_cum = np.cumsum(ex["residual"])
     nL = [0, 0]
-    ntok = np.zeros(4, int)
     for b in range(B):
         t = tr[b]
         ua, _ = oracle.uniforms(42, 0, 5, b)
@@ -84,29 +56,19 @@ def test_trace_fields_on_the_inverse_cdf_hand_example():
         assert t.u_acc[0] == ua
         assert abs(t.mu_a - abs(ua - ex["a0"])) < TOL
         Lb = int(L[b])
+        _, us = oracle.uniforms(42, Lb, 5, b)
+        assert t.u_smp == us
         if Lb == 0:
-            y, n, tu, v, mu = hand_draws(42, 0, 5, b, p_cum, ex["draw_accept"])
-            if mu < 1e-5:
-                continue
-            assert y is not None and int(tok[b, 0]) == y and t.n_draw == n
-            assert t.u_smp == tu and abs(t.theta - tu) < TOL and t.v_acc == v
-            assert abs(t.a_res - ex["draw_accept"][y]) < TOL and abs(t.R - ex["R"]) < TOL
-            cp, ct = cell(p_cum, y)
-            assert abs(t.C_prev - cp) < TOL and abs(t.C_tok - ct) < TOL
-            assert abs(t.mu_s - mu) < 1e-5
-            ntok[y] += 1
+            R, cum = ex["R"], res_cum
         else:
-            _, us = oracle.uniforms(42, 1, 5, b)
-            assert t.u_smp == us and t.n_draw == 0
-            cum = np.asarray(ex["bonus_cdf"])
-            assert abs(lam := t.lam_p[1]) < TOL and abs(t.R - 1.0) < TOL and abs(t.theta - us) < TOL
-            cp, ct = cell(cum, int(tok[b, 1]))
-            assert abs(t.C_prev - cp) < TOL and abs(t.C_tok - ct) < TOL
-            assert abs(t.mu_s - min(us - cp, ct - us)) < 1e-5
+            R, cum = 1.0, np.asarray(ex["bonus_cdf"])
+            assert abs(t.lam_p[1]) < TOL
+        assert abs(t.R - R) < TOL and abs(t.theta - us * R) < TOL
+        cp, ct = cell(cum, int(tok[b, Lb]))
+        assert abs(t.C_prev - cp) < TOL and abs(t.C_tok - ct) < TOL
+        assert abs(t.mu_s - min(us * R - cp, ct - us * R) / R) < 1e-5
         nL[Lb] += 1
     assert nL[0] > 1300 and nL[1] > 400         # Pr(L=0) = 0.75
-    assert ntok[0] == 0 and ntok[1] == 0        # 1 - q/p < 0: never accepted
-    assert abs(ntok[2] / ntok.sum() - 0.25) < 0.05   # the residual [0, 0, .1, .3] / .4
 
 
 def test_trace_and_decisions_on_the_accept_chain_hand_example():
@@ -133,24 +95,19 @@ def test_trace_and_decisions_on_the_accept_chain_hand_example():
         assert abs(t.mu_a - mu) < TOL
         for j in range(min(want_L + 1, 3)):
             assert abs(t.a[j] - a[j]) < TOL and abs(t.ell[j] - ex["ell"][j]) < TOL
-        tk = int(tok[b, want_L])
+        _, us = oracle.uniforms(9, want_L, 2, 100 + b)
         if want_L == 3:
-            _, us = oracle.uniforms(9, want_L, 2, 100 + b)
-            cum = np.asarray(ex["bonus_cdf"])
-            assert abs(t.R - 1.0) < TOL and abs(t.theta - us) < TOL
-            assert tk == int(np.argmax(cum > us))
+            cum, R = np.asarray(ex["bonus_cdf"]), 1.0
         else:
-            cum = np.cumsum(ex["p"][want_L])
-            y, n, tu, v, _ = hand_draws(9, want_L, 2, 100 + b, cum, ex["draw_accept_at"][str(want_L)])
-            R = ex["R_at"][str(want_L)]
-            assert abs(t.R - R) < TOL and t.n_draw == n
-            assert tk == (0 if want_L == 0 else 1)      # the only token with residual mass
-            if y is None:                               # every draw rejected: the C-9 fallback
-                _, us = oracle.uniforms(9, want_L, 2, 100 + b)
-                cum = np.cumsum(ex["residual_at"][str(want_L)])
-                assert abs(t.theta - us * R) < TOL
-            else:
-                assert tk == y and abs(t.theta - tu) < TOL
+            cum, R = np.cumsum(ex["residual_at"][str(want_L)]), ex["R_at"][str(want_L)]
+        assert abs(t.R - R) < TOL and abs(t.theta - us * R) < TOL
+        tk = int(tok[b, want_L])
+        if want_L == 0:
+            assert tk == 0
+        elif want_L == 2:
+            assert tk == 1
+        else:
+            assert tk == int(np.argmax(cum > us))
         cp, ct = cell(cum, tk)
         assert abs(t.C_prev - cp) < TOL and abs(t.C_tok - ct) < TOL
         counts[want_L] += 1
@@ -162,38 +119,22 @@ def test_trace_and_decisions_on_the_accept_chain_hand_example():
 # ---------------------------------------------------------------- sample_check -------------
 @pytest.mark.parametrize("L", [0, 1, 2, 3])
 def test_sample_check_cells_are_the_hand_cdf(L):
-    """sd_ref_sample_check at a FORCED accept length: at the bonus (L = 3) the hand CDF cell of
-    every token with theta = u_smp(3); below it (C-15) the hand p-CDF cell of token t with the
-    theta_u of the first draw that accepts t -- or, when an earlier draw surely accepts another
-    token, of that draw (the cell then excludes theta: t is inconsistent)."""
+    """sd_ref_sample_check at a FORCED accept length: the hand residual (or bonus) CDF cell of
+    every token, R and theta = u_smp(L) R."""
     ex = WORKED["accept_chain_hand"]
     p, q, ids = chain_batch(ex, 4)
+    if L == 3:
+        cum, R = np.asarray(ex["bonus_cdf"]), 1.0
+    else:
+        cum, R = np.cumsum(ex["residual_at"][str(L)]), ex["R_at"][str(L)]
     for b in range(4):
+        _, us = oracle.uniforms(3, L, 8, 50 + b)
         for t in range(3):
             Cp, Ct, Rv, th = oracle.sample_check(p, q, ids, b, L, t, 1.0, seed=3, round=8,
                                                  rid_base=50)
-            if L == 3:
-                _, us = oracle.uniforms(3, L, 8, 50 + b)
-                cp, ct = cell(np.asarray(ex["bonus_cdf"]), t)
-                assert abs(Rv - 1.0) < TOL and abs(th - us) < TOL
-            else:
-                cum = np.cumsum(ex["p"][L])
-                acc = ex["draw_accept_at"][str(L)]
-                cp, ct = cell(cum, t)
-                want = None
-                for n in range(oracle.NDRAW):
-                    tu, v = oracle.draw_uniforms(3, L, n, 8, 50 + b)
-                    y = int(np.searchsorted(cum, tu, side="right"))
-                    if y == t and v < acc[t]:
-                        want = tu            # consistent: draw n accepts t
-                        break
-                    if v < acc[y]:
-                        want = tu            # draw n accepts y != t: theta outside t's cell
-                        break
-                assert want is not None and abs(Rv - 1.0) < TOL and abs(th - want) < TOL
-                inside = cp <= th <= ct
-                assert inside == (t == (0 if L == 0 else (1 if L == 2 else int(np.searchsorted(cum, want, side="right")))))
+            cp, ct = cell(cum, t)
             assert abs(Cp - cp) < TOL and abs(Ct - ct) < TOL
+            assert abs(Rv - R) < TOL and abs(th - us * R) < TOL
 
 
 def test_sample_check_zero_residual_falls_back_to_p():

@@ -33,12 +33,6 @@ def tree_from_tables(P, Q, m, d, cand):
 
 
 def test_m1_tree_is_the_chain():
-    """m = 1 is the chain: identical accept lengths, statuses, accepted prefixes and bonus tokens
-    (same Philox counters).  The correction token is drawn differently -- the chain by C-15's
-    rejection draws, the tree by D-2's inverse CDF of the residual (with the chain's fallback
-    uniform) -- so there it must be the chain's C-15 fallback token when the chain took the
-    fallback, and a token of positive residual mass (scipy softmax) otherwise."""
-    from scipy import special
     d = make_batch(V=200, k=4, B=300, T=1.0, kappa=10.0, seed=5)
     B, k = d["ids"].shape
     tok = np.zeros((B, k + 1), np.int32)
@@ -46,20 +40,11 @@ def test_m1_tree_is_the_chain():
     for T in (1.0, 0.0):
         L, toks, st, node, mu = oracle.tree_verify(d["p"], d["q"] if T else None, tok, 1, k, T,
                                                    seed=9, round=3, rid_base=70)
-        rL, rtok, rst, tr = oracle.verify(d["p"], d["q"] if T else None, d["ids"], T, seed=9,
-                                          round=3, rid_base=70, trace=True)
+        rL, rtok, rst = oracle.verify(d["p"], d["q"] if T else None, d["ids"], T, seed=9, round=3,
+                                      rid_base=70)
         np.testing.assert_array_equal(L, rL)
+        np.testing.assert_array_equal(toks, rtok)
         np.testing.assert_array_equal(st, rst)
-        for b in range(B):
-            Lb = int(L[b])
-            np.testing.assert_array_equal(toks[b, :Lb], rtok[b, :Lb])
-            np.testing.assert_array_equal(toks[b, Lb + 1:], rtok[b, Lb + 1:])
-            if T == 0 or Lb == k or tr[b].n_draw == oracle.NDRAW + 1:
-                assert toks[b, Lb] == rtok[b, Lb]
-            else:
-                pp = special.softmax(d["p"][b, Lb].astype(np.float64) / T)
-                qq = special.softmax(d["q"][b, Lb].astype(np.float64) / T)
-                assert pp[toks[b, Lb]] > qq[toks[b, Lb]] and pp[rtok[b, Lb]] > qq[rtok[b, Lb]]
 
 
 @pytest.mark.parametrize("V,m,d", [(3, 2, 2), (4, 3, 1)])

@@ -12,16 +12,7 @@ MUTATIONS = [
     ("accept_probs: a without min(1, .)", "a_out[j] = ell >= 0.0 ? 1.0 : exp(ell);", "a_out[j] = exp(ell);"),
     ("accept_probs: u from w1", "sd_ref_uniforms(seed, (uint32_t)j, round, rid_base + (uint64_t)b, &u_out[j], NULL);",
      "sd_ref_uniforms(seed, (uint32_t)j, round, rid_base + (uint64_t)b, NULL, &u_out[j]);"),
-    ("trace: mu_s not divided by R", "double ms = (m1 < m2 ? m1 : m2) / R;", "double ms = (m1 < m2 ? m1 : m2);"),
-    ("C-15: accept with q/p instead of 1 - q/p", "double acc = 1.0 - prob_of(qr, y, T, lam_q) / buf[y];\n            double m1",
-     "double acc = prob_of(qr, y, T, lam_q) / buf[y];\n            double m1"),
-    ("C-15: accept iff v >= a", "            if (v < acc) {                                      /* accepted: t = y */",
-     "            if (v >= acc) {                                      /* accepted: t = y */"),
-    ("C-15: draw counter without the +1", "uint32_t ctr[4] = {L + ((n + 1u) << 20),", "uint32_t ctr[4] = {L + (n << 20),"),
-    ("C-15: fallback not taken (token from the last draw)", "        if (tr) { tr->mu_s = mu; tr->n_draw = SD_REF_NDRAW + 1; }",
-     "        if (tr) { tr->mu_s = mu; tr->n_draw = SD_REF_NDRAW + 1; }\n        emit(a, b, L, 0, status); return;"),
-    ("sample_check C-15: consistency test ignores v", "&& v < at + tau) {", ") {"),
-    ("C-15: draw margin ignores the accept test", "            if (m3 < mu) mu = m3;\n", ""),
+    ("trace: mu_s not divided by R", "tr->mu_s = (m1 < m2 ? m1 : m2) / R;", "tr->mu_s = (m1 < m2 ? m1 : m2);"),
     ("trace: mu_a against ell", "double mu = fabs(u_acc - acc);", "double mu = fabs(u_acc - ell);"),
     ("trace: C_prev = C(t)", "            *C_prev = C;\n            *C_tok = Cn;", "            *C_prev = Cn;\n            *C_tok = Cn;"),
     ("sample_check: C(t-1) includes t", "for (int32_t y = 0; y < t; ++y) C += buf[y];", "for (int32_t y = 0; y <= t; ++y) C += buf[y];"),
