@@ -324,8 +324,6 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # workspace word 1: requests whose residual sample the fused chunk tasks took (include/starsd.h)
-    fused0 = int(ws.buf[4:8].view(torch.int32).item())
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -337,7 +335,6 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1)
-    fused_n = (int(ws.buf[4:8].view(torch.int32).item()) - fused0) % (1 << 32)
     tsh = ts.cpu().numpy().view(np.uint64)
     gp.replay()                      # the evented replay: k_row_stats event pairs (cross-check)
     torch.cuda.synchronize()
@@ -461,8 +458,7 @@ def run_ours(args):
             "kernel_plan": pl,
             "clocks": clocks,
             "accept": {"mean_L": float(Lh.mean()), "mean_emitted": float((Lh + 1).mean()),
-                       "fault_requests": int((~ok).sum()),
-                       "fused_sampled_frac": fused_n / float(K * B)},
+                       "fault_requests": int((~ok).sum())},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -107,9 +107,8 @@ typedef struct {
  *   out_status    device, [B] int32 fault bitmask, or NULL
  *   workspace     device, >= sd_verify_workspace_size() bytes, 16-byte aligned, zero-filled
  *                 once before its first use.  Every call leaves the zero region of its shape
- *                 zeroed again (words 0 and 1 excepted: 32-bit counters the kernels keep -- word
- *                 0 counts calls, word 1 counts requests whose residual sample was taken inside
- *                 the statistics kernel by fused sampling chunk tasks; both wrap); the library
+ *                 zeroed again (word 0 excepted: a 32-bit counter of calls the kernels keep, it
+ *                 wraps); the library
  *                 remembers, per workspace pointer in this process, the layout of the last call
  *                 it enqueued there, and a call of another shape (batch, k, vocab, dtype, T == 0
  *                 or not) first zero-fills the union of both zero regions on `stream` (a
@@ -158,10 +157,9 @@ sd_status sd_verify_workspace_size(const sd_shape* shape, float temperature, siz
  *   ctas         CTAs of k_row_stats; tail_ctas: CTAs of the second kernel
  *   tagged       rows publish tagged partials to a start-ticket decider (2..64 chunks per row)
  *   options      SD_PLAN_* bits of the scheduling options in effect (environment knobs read once
- *                per process): PIPE = k_row_pipe replaces k_row_stats
- *                (ctas = its persistent grid), EARLY = k_sample_req launched during the last
- *                position wave (tail_ctas includes its completion probe), FUSED = fused sampling
- *                chunk tasks
+ *                per process): EARLY = k_sample_req launched during the last
+ *                position wave (tail_ctas includes its completion probe).  Bits 1 and 4 (PIPE,
+ *                FUSED) are retired: those opt-in variants measured slower and were removed.
  */
 enum { SD_PLAN_PIPE = 1, SD_PLAN_EARLY = 2, SD_PLAN_FUSED = 4 };
 enum { SD_VARIANT_TWO_LAUNCH = 1 };

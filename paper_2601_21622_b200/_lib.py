@@ -41,7 +41,7 @@ class Plan(ctypes.Structure):
                 ("tail_ctas", ctypes.c_int64), ("tagged", ctypes.c_int32), ("options", ctypes.c_int32)]
 
 
-PLAN_OPTIONS = {1: "pipe", 2: "early", 4: "fused"}
+PLAN_OPTIONS = {2: "early"}
 
 
 VARIANT_NAMES = {1: "two_launch"}

@@ -167,22 +167,9 @@ static void fill_params(Params& P, const sd_shape* shape, int esz, float tempera
     static const int chain = env_flag("STARSD_CHAIN", 1);   // 0: plain stream order
     P.chain = chain ? 1 : 0;
     P.esz = esz;
-    P.claimed = reinterpret_cast<unsigned long long*>(ws + w.claimed);
-    // fused sampling: chunks of exactly one 32-segment block (16 KB), at most 63 of them per row
-    // (opt-in: measured slower at c3 -- the stop rows are L2-cold one position wave later,
-    // profiles/README.md r02)
-    static const int fs = env_flag("STARSD_FUSED_SAMPLE", 0);   // A/B knob
-    P.fsample = (fs && !greedy && P.k >= 1 && P.CH * esz == 16 * 1024 &&
-                 P.nch <= 63) ? 1 : 0;
-    static const int pipe = env_flag("STARSD_PIPE", 0);         // A/B knob
-    P.pipe = (pipe && P.nch >= 9 && P.nch <= kMaxTagNch && P.CH * esz <= kMaxChunkBytes) ? (pipe == 2 ? 2 : 1) : 0;
-    if (P.pipe) {
-        P.tagpub = 1;   // (tagged partials; the second kernel advances the call counter)
-        P.fsample = 0;
-    }
     static const int early = env_flag("STARSD_EARLY", 1);       // A/B knob
     const int64_t nseg_row = (static_cast<int64_t>(P.V) + 32 * (16 / esz) - 1) / (32 * (16 / esz));
-    P.early = (early && !greedy && !P.fsample && P.chain &&
+    P.early = (early && !greedy && P.chain &&
                nseg_row <= 2048) ? 1 : 0;   // (k_sample_req's on-chip table: kSMaxSeg)
     static const int rg = env_flag("STARSD_RGROUP", 0);          // A/B knob
     P.rgroup = rg > 0 ? rg : 0;
@@ -251,8 +238,6 @@ static sd_status verify_impl(const void* p_logits, const void* q_logits, const Q
         P.p_stage = p_stage;
         P.q_stage = q_stage;
         P.early = 0;
-        P.fsample = 0;
-        P.pipe = 0;
     }
     P.seed = seed;
     P.round = round;
@@ -493,15 +478,7 @@ sd_status sd_verify_plan(const sd_shape* shape, float temperature, sd_plan* out)
     Params P{};
     alignas(16) static char dummy[16];
     fill_params(P, shape, esz, temperature, dummy);
-    out->options = (P.pipe ? SD_PLAN_PIPE : 0) | (P.early ? SD_PLAN_EARLY : 0) |
-                   (P.fsample ? SD_PLAN_FUSED : 0);
-    if (P.pipe) {
-        int dev = 0, sms = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess &&
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
-            out->ctas = static_cast<int64_t>(sms) * (P.pipe == 2 ? 2 : 1);
-        out->tagged = 1;
-    }
+    out->options = P.early ? SD_PLAN_EARLY : 0;
     if (P.early) out->tail_ctas += 1;
     return SD_OK;
 }

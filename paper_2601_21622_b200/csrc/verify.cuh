@@ -109,16 +109,9 @@ struct Params {
     int32_t esz;                 // bytes per logit
     const QMeta* qmeta;          // [B][k] draft-row metadata: the q rows are then read only at the
                                  // stop position (sd_verify_qmeta); NULL: full q rows
-    // fused sampling (fsample): a k_row_stats CTA of position j > L whose request is settled at L
-    // runs sampling chunk task c of row L (claimed in claimed[b]) while that row is still in L2;
-    // the request's last task searches and writes the outputs; k_sample_req only handles what is
-    // left (the bonus position, the C-6 retry, hard faults, a request settled too late)
-    int32_t fsample;
-    unsigned long long* claimed; // [B] bits 0..62: chunk task c claimed; bit 63: outputs written
     int32_t early;               // k_sample_req launched during k_row_stats' last position wave
     void* p_stage;               // sd_verify_staged: device copies of the rows k_row_stats reads
     void* q_stage;               // (the sampling kernels then read their stop rows from here)
-    int32_t pipe;                // k_row_pipe (pipelined persistent CTAs) instead of k_row_stats
     int32_t rgroup;              // k_row_stats grid: requests per group (grid order: group-major,
                                  // then position, request, chunk); B = one group (position-major)
 };
@@ -149,7 +142,7 @@ inline int32_t row_cluster(int32_t nch) {
 // Workspace layout for a shape; all offsets 16-byte aligned.  The first `zero_bytes` must be
 // zero before a call and are zero again after it (word 0, the call counter, excepted).
 struct WsLayout {
-    size_t epoch, state, ticketA, ticketB, tailT, claimed, zero_bytes;
+    size_t epoch, state, ticketA, ticketB, tailT, zero_bytes;
     size_t rowstat, partA, partB, segtab, rres, partT, total;
 };
 
@@ -178,7 +171,6 @@ inline WsLayout ws_layout(int32_t B, int32_t k, int32_t V, int32_t esz) {
     w.ticketA = o;  o = align16(o + sizeof(uint32_t) * (size_t)B * (k + 1));
     w.ticketB = o;  o = align16(o + sizeof(uint32_t) * B);
     w.tailT = o;    o = align16(o + sizeof(uint32_t) * B);
-    w.claimed = o;  o = align16(o + sizeof(unsigned long long) * B);
     w.zero_bytes = o;
     w.rowstat = o;  o = align16(o + sizeof(RowStat) * (size_t)B * (k + 1));
     w.partA = o;    o = align16(o + sizeof(PartA) * (size_t)B * (k + 1) * nch);

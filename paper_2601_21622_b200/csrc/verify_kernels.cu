@@ -13,12 +13,7 @@
 //                 decides the acceptance test and ORs "decided" (and "stopped") bits into the
 //                 request's 64-bit state word.
 //                 A CTA whose request already stopped below j skips its load (laziness, SURVEY
-//                 8(d)).  If the request is SETTLED at L = j - 1 (positions 0..L decided, L the
-//                 first stop), that CTA instead runs sampling chunk task c of row L: it re-reads
-//                 chunk c of (p_L, q_L) -- read one position wave earlier, so from L2 --, computes
-//                 r = max(0, p - q) per 32-vector segment (fp64 masses) and publishes them; the
-//                 request's last chunk task runs the inverse-CDF search chunk -> segment -> token
-//                 and writes the outputs.
+//                 8(d)).
 //   k_sample_req  one CTA per request streams its stop row pair (p_L, q_L) -- or p_k for the
 //                 bonus -- through a TMA ring, computes the residual segment masses on chip and
 //                 runs the inverse-CDF search (k_sample_chunked for vocabularies beyond its
@@ -289,10 +284,6 @@ __device__ __forceinline__ void write_outputs(const Params& P, int b, int L, int
 __device__ __forceinline__ void reset_request(const Params& P, int b) {
     P.state[b] = 0ull;
     for (int i = 0; i <= P.k; ++i) P.ticketA[static_cast<size_t>(b) * (P.k + 1) + i] = 0u;
-    if (P.fsample) {
-        P.ticketB[b] = 0u;
-        P.claimed[b] = 0ull;
-    }
 }
 
 // Combination of n slice partials (fp64, exact 2^(D_c - D) rescales); warp-collective, the
@@ -1014,90 +1005,6 @@ __device__ __forceinline__ void sample_task(const Params& P, unsigned char* smem
     }
 }
 
-// Fused sampling chunk task (k_row_stats with P.fsample; whole CTA): chunk c of request b's stop
-// row pair (p_L, q_L), L < k, staged into this CTA's shared memory -- from L2 when the row was
-// read one position wave earlier -- and reduced exactly as k_sample_req reduces it: the scaled
-// residual terms of every 16-byte vector (resid_scaled), one fp64 warp tree sum per 32-vector
-// segment, the chunk's mass (the chunk is one 32-segment block) as the warp tree sum of its
-// segment masses.  The CTA completing the request's last task runs the same inverse-CDF search
-// (cdf_search_blocks / cdf_search_segment) over the published masses, writes the outputs and sets
-// bit 63 of claimed[b]; a zero residual (C-6) is left to k_sample_req's retry.
-template <typename E>
-__device__ __forceinline__ void fused_sample_task(const Params& P, unsigned char* smem, uint64_t* bar,
-                                                  double* s_seg, int* s_last, int b, int L, int c,
-                                                  const RowStat& rs) {
-    using EL = Elt<E>;
-    constexpr int VEC = EL::VEC;
-    constexpr int SEGV = 32;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int kk = P.k, V = P.V, nch = P.nch;
-    const E* gp = static_cast<const E*>(P.p_stage ? P.p_stage : P.p) + (static_cast<int64_t>(b) * (kk + 1) + L) * P.ld_p;
-    const E* gq = static_cast<const E*>(P.q_stage ? P.q_stage : P.q) + (static_cast<int64_t>(b) * kk + L) * P.ld_q;
-    const int vpc = P.CH / VEC;                        // vectors per chunk (32 segments)
-    const int nvv = (V + VEC - 1) / VEC;               // vectors of the row
-    const int v0 = c * vpc;
-    const int nvc = min(vpc, nvv - v0);                // vectors of this chunk
-    const uint32_t bytes = static_cast<uint32_t>(nvc) * 16u;   // (row strides are 16-byte padded)
-    unsigned char* sq = smem + static_cast<size_t>(P.CH) * sizeof(E);
-    if (tid == 0) {
-        mbar_arrive_expect_tx(&bar[0], bytes);
-        bulk_g2s(smem, reinterpret_cast<const uint4*>(gp) + v0, bytes, &bar[0]);
-    } else if (tid == 32) {
-        mbar_arrive_expect_tx(&bar[1], bytes);
-        bulk_g2s(sq, reinterpret_cast<const uint4*>(gq) + v0, bytes, &bar[1]);
-    }
-    const float c2 = P.c2, nDp = -rs.M_p, nDq = -rs.M_q;
-    const float rho = static_cast<float>(rs.S_p / rs.S_q);
-    mbar_wait(&bar[0], 0u);
-    mbar_wait(&bar[1], 0u);
-    const uint4* sp4 = reinterpret_cast<const uint4*>(smem);
-    const uint4* sq4 = reinterpret_cast<const uint4*>(sq);
-#pragma unroll
-    for (int i = 0; i < 32 / kWarps; ++i) {
-        const int sg = warp + i * kWarps;
-        const int gl = sg * SEGV + lane, g = v0 + gl;
-        uint4 up = make_uint4(0u, 0u, 0u, 0u), uq = up;
-        if (gl < nvc) {
-            up = sp4[gl];
-            uq = sq4[gl];
-        }
-        const int valid = g < nvv - 1 ? VEC : min(VEC, max(0, V - g * VEC));
-        float r[VEC];
-        const double m =
-            warp_sum(static_cast<double>(resid_scaled<E>(up, uq, valid, c2, nDp, nDq, rho, r)));
-        if (lane == 0) s_seg[sg] = m;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        const double m = s_seg[lane];
-        const double t = warp_sum(m);
-        P.segtab[(static_cast<size_t>(b) * nch + c) * 32 + lane].x = m;
-        if (lane == 0) P.partB[static_cast<size_t>(b) * nch + c].R = t;
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) *s_last = atomicAdd(P.ticketB + b, 1u) == static_cast<uint32_t>(nch - 1);
-    __syncthreads();
-    if (!*s_last || warp != 0) return;
-    __threadfence();
-    const uint4 w = verify_words(P.seed, static_cast<uint32_t>(L), P.round,
-                                 P.rid_base + static_cast<uint64_t>(b));
-    int sgsel = 0;
-    double th2 = INFINITY;
-    const double tot = cdf_search_blocks(
-        [&](int i) { return __ldcg(&P.partB[static_cast<size_t>(b) * nch + i].R); },
-        [&](int i) { return __ldcg(&P.segtab[(static_cast<size_t>(b) * nch + (i >> 5)) * 32 + (i & 31)].x); },
-        nch, (nvv + SEGV - 1) / SEGV, w.y, lane, &sgsel, &th2);
-    if (!(tot > 0.0)) return;   // C-6: k_sample_req retries with p_L
-    const int32_t tok = cdf_search_segment<E>(gp, gq, sgsel, th2, V, nvv, c2, nDp, nDq, rho, lane);
-    if (lane == 0) {
-        write_outputs(P, b, L, tok, rs.status, false);
-        P.rres[b] = tot / rs.S_p;   // (trace) mass of the distribution sampled
-        atomicOr(P.claimed + b, 1ull << 63);
-        SD_TRF(P, 8);
-    }
-}
-
 // The slice partial of one chunk (whole CTA; valid in warp 0, zx fields in lane 0): wait for the
 // bulk copies (mbarrier parities ph0 / ph1), unpack NV vectors per thread into registers, the lean
 // statistics (or argmax) per thread, warp and block reductions.
@@ -1269,10 +1176,9 @@ __global__ void __launch_bounds__(kThreads, rs_min_blocks(GREEDY, sizeof(E))) k_
     __shared__ __align__(16) PartA s_parts[CL];
     __shared__ __align__(16) PartA s_all[TAG ? kMaxTagNch : 1]; // TAG: the row's partials
     __shared__ uint32_t s_tag;
-    __shared__ int s_flag, s_L, s_last;
+    __shared__ int s_flag;
     __shared__ float s_d[2][kWarps];
     __shared__ double s_s[2][kWarps];
-    __shared__ double s_seg[GREEDY ? 1 : 32];
     __shared__ int s_gi[kWarps], s_f[kWarps];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1301,24 +1207,9 @@ __global__ void __launch_bounds__(kThreads, rs_min_blocks(GREEDY, sizeof(E))) k_
     if (P.prof_ts && tid == 0 && blockIdx.y == 0 && blockIdx.z == 0) prof_min(P.prof_ts);
     if (tid == 0) {
         SD_TR(P, 0);
-        const bool fs = !GREEDY && P.fsample && j > 0 && c < nch;
         const unsigned long long s = j ? ld_relaxed_u64(P.state + b) : 0ull;
-        const unsigned long long cl = fs ? ld_relaxed_u64(P.claimed + b) : 0ull;
         const uint32_t m = static_cast<uint32_t>(s >> 32);
-        const bool skip = (m & ((1u << j) - 1u)) != 0u;
-        // fused sampling: a request settled at L < j whose chunk task c is unclaimed -- this CTA
-        // claims it (the first position wave after L normally claims every chunk)
-        int tL = -1;
-        if (fs && skip) {
-            const int L = settled_L(s, kk);
-            const unsigned long long bit = 1ull << c;
-            if (L >= 0 && !(cl & bit) && !(atomicOr(P.claimed + b, bit) & bit)) {
-                tL = L;
-                __threadfence();   // acquire: row L's rowstat, released with the state bits
-            }
-        }
-        s_L = tL;
-        s_flag = skip;
+        s_flag = (m & ((1u << j) - 1u)) != 0u;
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         if (CL > 1 && rank == 0) mbar_init(&s_pbar, 1);
@@ -1346,13 +1237,6 @@ __global__ void __launch_bounds__(kThreads, rs_min_blocks(GREEDY, sizeof(E))) k_
                 } else {
                     spin_until([&] { return mbar_try_wait_cluster(&s_pbar, 0); }, 2);
                 }
-            }
-        }
-        if constexpr (!GREEDY) {
-            if (s_L >= 0) {   // fused sampling chunk task c of row L
-                const RowStat rs = load_cg(P.rowstat + static_cast<size_t>(b) * (kk + 1) + s_L);
-                if (!(rs.status & kHard))
-                    fused_sample_task<E>(P, smem, bar, s_seg, &s_last, b, s_L, c, rs);
             }
         }
         return;
@@ -1469,443 +1353,6 @@ __global__ void __launch_bounds__(kThreads, rs_min_blocks(GREEDY, sizeof(E))) k_
 
 
 // ------------------------------------------------------------------------------------------
-// Kernel A, pipelined persistent form (k_row_pipe; rows of 1..64 chunks, P.pipe): one CTA per SM
-// streams the same work items as k_row_stats' grid -- (chunk c, request b, position j),
-// position-major -- through a TMA ring, with the control round trips of the per-item kernel taken
-// off the data path by warp specialisation:
-//   producer warp   items blockIdx.x + m * gridDim.x in order (static assignment: no claim
-//                   atomics); the request state words of the next kPipeBatch items are loaded one
-//                   batch ahead (laziness test), a skipped item's tagged "skipped" partial is
-//                   stored at once, a needed one gets a ring slot: lane 0 copies the p chunk, lane 1
-//                   the q chunk (16 KB bulk copies on the slot's two mbarriers);
-//   2 x 8 consumer  warp groups take ring entries alternately: unpack the slot into registers,
-//                   release it, the lean statistics, block reduction behind a named barrier, the
-//                   chunk partial into a shared queue (identical arithmetic to k_row_stats);
-//   publisher warp  queue entries in order: a chunk's partial as ten tagged words (no fence, no
-//                   ticket); the row's last chunk (c = nch - 1) polls the row's other partials,
-//                   combines and decides.
-// Progress: a decider waits only on items of smaller global index; each CTA publishes its items
-// in increasing index order and every CTA is resident (grid = SMs x 1), so every wait chain runs
-// to strictly smaller indices and ends -- no dispatch-order assumption, no cycle; the waits are
-// bounded anyway (spin_until -> SD_FAULT_PROTOCOL).
-// volatile shared-memory reads (values another warp stored, ordered by a block fence + atomic)
-__device__ __forceinline__ int ld_volatile_i32(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
-__device__ __forceinline__ float ld_volatile_f32(const float* p) { return *reinterpret_cast<const volatile float*>(p); }
-__device__ __forceinline__ double ld_volatile_f64(const double* p) { return *reinterpret_cast<const volatile double*>(p); }
-
-// A ring wait of k_row_pipe: local TMA / warp handoffs that complete in microseconds in a correct
-// run.  A broken invariant must not hang the GPU: after 2 s the kernel traps (the launch fails with
-// an error on the stream) instead of spinning forever.
-__device__ __forceinline__ void pipe_wait(uint64_t* bar, uint32_t parity) {
-    if (mbar_try_wait(bar, parity)) return;
-    const unsigned long long t0 = gtimer();
-    for (uint32_t k = 1;; ++k) {
-        if (mbar_try_wait(bar, parity)) return;
-        if ((k & 1023u) == 0u && gtimer() - t0 > 2000ull * 1000 * 1000) __trap();
-    }
-}
-// NG consumer warp groups per CTA: NG = 3 -> one CTA per SM with a 192 KB ring; NG = 2 -> two
-// CTAs per SM with 96 KB rings each (<= 53 registers per thread)
-template <int NG> __host__ __device__ constexpr int pipe_threads() { return (NG * kWarps + 3) * 32; }   // + 3 warps
-template <int NG> __host__ __device__ constexpr int pipe_ring() { return NG == 3 ? 192 * 1024 : 96 * 1024; }
-template <int NG> __host__ __device__ constexpr int pipe_cps() { return NG == 3 ? 1 : 2; }              // CTAs per SM
-constexpr int kPipeDQ = 32;                                     // pending row decisions
-constexpr int kPipeNQ = 12;                                     // partial queue entries (groups | NQ)
-constexpr int kPipeBatch = 4;                                   // state words loaded together
-struct PipeEntry {
-    PartA a;
-    int32_t c, b, j, x;   // c < 0: end of the CTA's items
-};
-
-template <typename E, bool GREEDY, int NG>
-__global__ void __launch_bounds__(pipe_threads<NG>(), pipe_cps<NG>()) k_row_pipe(const Params P) {
-    constexpr int kPipeGroups = NG;
-    constexpr int kPipeRingBytes = pipe_ring<NG>();
-    using EL = Elt<E>;
-    constexpr int VEC = EL::VEC;
-    constexpr int NV = kMaxChunkBytes / kVecBytes / kThreads;   // 16-byte vectors per thread
-    constexpr int SLOT = (GREEDY ? 1 : 2) * kMaxChunkBytes;     // one chunk of p (and of q)
-    constexpr int NS = kPipeRingBytes / SLOT;                   // 6 slots (12 greedy)
-    static_assert(2 * NS <= 32, "one issuing lane pair per ring slot");
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t full[NS][2], empty[NS], pq_full[kPipeNQ], pq_empty[kPipeNQ];
-    __shared__ __align__(8) uint64_t dq_full[kPipeDQ], dq_empty[kPipeDQ];
-    __shared__ int4 dq[kPipeDQ];                                // (b, j, x, end) of a row to decide
-    __shared__ int4 meta[NS];                                   // (c, b, j, x) of the slot's entry
-    __shared__ __align__(16) PipeEntry pq[kPipeNQ];
-    __shared__ __align__(16) PartA s_all[kMaxTagNch];
-    constexpr int RB = 4;                                       // reduction scratch per group
-    __shared__ float r_d[kPipeGroups][RB][2][kWarps];
-    __shared__ double r_s[kPipeGroups][RB][2][kWarps];
-    __shared__ int r_gi[kPipeGroups][RB][kWarps], r_f[kPipeGroups][RB][kWarps];
-    __shared__ float r_zx[kPipeGroups][RB][2];
-    __shared__ uint32_t r_cnt[kPipeGroups][RB];                // warps that stored their partial
-    __shared__ uint32_t s_tag;
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nch = P.nch, kk = P.k, B = P.B;
-    if (tid == 0) {
-        for (int i = 0; i < NS; ++i) {
-            mbar_init(&full[i][0], 1);
-            mbar_init(&full[i][1], 1);
-            mbar_init(&empty[i], kWarps);
-        }
-        for (int i = 0; i < kPipeNQ; ++i) {
-            mbar_init(&pq_full[i], 1);
-            mbar_init(&pq_empty[i], 1);
-        }
-        for (int i = 0; i < kPipeDQ; ++i) {
-            mbar_init(&dq_full[i], 1);
-            mbar_init(&dq_empty[i], 1);
-        }
-        fence_mbar_init();
-    }
-    if (tid < kPipeGroups * RB) (&r_cnt[0][0])[tid] = 0u;
-    if (P.chain) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (tid == 0) {
-        s_tag = (ld_relaxed_u32(P.epoch) + 1u) | 0x80000000u;
-        if (P.prof_ts && blockIdx.x == 0) prof_min(P.prof_ts);
-    }
-    __syncthreads();
-    const uint32_t tag = s_tag;
-    constexpr int PW = kPipeGroups * kWarps, QW = PW + 1, DW = PW + 2;
-
-    if (warp == PW) {
-        // ---------------------------------------------------------------- producer warp
-        // lane l < kPipeBatch walks items blockIdx.x + (m kPipeBatch + l) gridDim.x as a (c, b, j)
-        // cursor (carry adds, no division in the loop); its request's state word and draft id
-        // for the next batch are loaded while the current batch issues
-        const long long per_pos = static_cast<long long>(nch) * B;
-        auto split = [&](long long i, int& c, int& b, int& j) {
-            j = static_cast<int>(i / per_pos);
-            const long long r = i - j * per_pos;
-            b = static_cast<int>(r / nch);
-            c = static_cast<int>(r - static_cast<long long>(b) * nch);
-        };
-        int c, b, j, sc, sb, sj;
-        split(blockIdx.x + static_cast<long long>(lane) * gridDim.x, c, b, j);
-        split(static_cast<long long>(kPipeBatch) * gridDim.x, sc, sb, sj);
-        if (lane >= kPipeBatch) j = kk + 1;                      // (no item)
-        auto load_words = [&](unsigned long long& st, int& x) {
-            st = 0ull;
-            x = -1;
-            if (j <= kk) {
-                if (j) st = ld_relaxed_u64(P.state + b);
-                if (j < kk) x = P.ids[static_cast<size_t>(b) * kk + j];
-            }
-        };
-        unsigned long long st_cur;
-        int x_cur;
-        load_words(st_cur, x_cur);
-        uint32_t n = 0;                                          // ring entries issued
-        while (__any_sync(0xFFFFFFFFu, j <= kk)) {
-            const int cc = c, cb = b, cj = j, cx = x_cur;
-            const bool valid = cj <= kk;
-            const bool skip = valid && cj && (static_cast<uint32_t>(st_cur >> 32) & ((1u << cj) - 1u));
-            if (skip) {
-                // the request stopped below j: the row is never needed (laziness); its decider
-                // must not wait for this chunk, so the chunk is published as skipped
-                unsigned long long* w = P.partT + ((static_cast<size_t>(cb) * (kk + 1) + cj) * nch + cc) * 10;
-                const unsigned long long hi = static_cast<unsigned long long>(tag) << 32;
-#pragma unroll
-                for (int q = 0; q < 10; ++q) {
-                    const unsigned long long v = hi | (q == 8 ? static_cast<uint32_t>(kPartSkipped) : 0u);
-                    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(w + q), "l"(v) : "memory");
-                }
-            }
-            unsigned need = __ballot_sync(0xFFFFFFFFu, valid && !skip);
-            if (j <= kk) {                                       // advance the cursor
-                c += sc;
-                const int k1 = c >= nch;
-                c -= k1 ? nch : 0;
-                b += sb + k1;
-                const int k2 = b >= B;
-                b -= k2 ? B : 0;
-                j += sj + k2;
-            }
-            unsigned long long st_nxt;
-            int x_nxt;
-            load_words(st_nxt, x_nxt);                           // (in flight while this batch issues)
-            while (need) {
-                const int l = __ffs(need) - 1;
-                need &= need - 1;
-                const int ic = __shfl_sync(0xFFFFFFFFu, cc, l), ib = __shfl_sync(0xFFFFFFFFu, cb, l);
-                const int ij = __shfl_sync(0xFFFFFFFFu, cj, l), ix = __shfl_sync(0xFFFFFFFFu, cx, l);
-                const int sl = static_cast<int>(n % NS);
-                if (n >= NS) pipe_wait(&empty[sl], ((n / NS) & 1u) ^ 1u);
-                // a different lane pair per slot: a thread's bulk copies complete one after
-                // another, so rotating issuers keeps every slot's copies in flight together
-                const int c0 = ic * P.CH;
-                const uint32_t bytes = static_cast<uint32_t>((min(P.CH, P.V - c0) + VEC - 1) / VEC) * 16u;
-                if (lane == 2 * sl) {
-                    meta[sl] = make_int4(ic, ib, ij, ix);
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    mbar_arrive_expect_tx(&full[sl][0], bytes);
-                    bulk_g2s(smem + static_cast<size_t>(sl) * SLOT,
-                             static_cast<const E*>(P.p) + (static_cast<int64_t>(ib) * (kk + 1) + ij) * P.ld_p + c0,
-                             bytes, &full[sl][0]);
-                } else if (lane == 2 * sl + 1) {
-                    if (!GREEDY && ij < kk && P.qmeta == nullptr) {
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        mbar_arrive_expect_tx(&full[sl][1], bytes);
-                        bulk_g2s(smem + static_cast<size_t>(sl) * SLOT + kMaxChunkBytes,
-                                 static_cast<const E*>(P.q) + (static_cast<int64_t>(ib) * kk + ij) * P.ld_q + c0,
-                                 bytes, &full[sl][1]);
-                    } else {
-                        mbar_arrive(&full[sl][1]);               // (every use advances the phase)
-                    }
-                }
-                ++n;
-            }
-            st_cur = st_nxt;
-            x_cur = x_nxt;
-        }
-        for (int t = 0; t < kPipeGroups; ++t, ++n) {              // one end marker per group
-            const int sl = static_cast<int>(n % NS);
-            if (n >= NS) pipe_wait(&empty[sl], ((n / NS) & 1u) ^ 1u);
-            if (lane == 0) {
-                meta[sl] = make_int4(-1 - t, 0, 0, 0);
-                mbar_arrive(&full[sl][0]);
-                mbar_arrive(&full[sl][1]);
-            }
-        }
-        // P.early: this CTA issued its last item; once every CTA has, the sampler may launch
-        if (P.early) asm volatile("griddepcontrol.launch_dependents;");
-        return;
-    }
-
-    if (warp == QW) {
-        // ---------------------------------------------------------------- publisher warp
-        // every chunk partial goes out as ten tagged words (no fence, no ticket); the row's last
-        // chunk (c = nch - 1) also queues the row for the decider warp, so waiting for the other
-        // chunks never stalls this CTA's pipeline
-        uint32_t nd = 0;                                         // rows queued for decision
-        for (uint32_t n = 0;; ++n) {
-            const int e = static_cast<int>(n % kPipeNQ);
-            pipe_wait(&pq_full[e], (n / kPipeNQ) & 1u);
-            const PipeEntry en = pq[e];
-            const bool end = en.c < 0;
-            if (!end && nch > 1 && lane < 10) {
-                const size_t pos = static_cast<size_t>(en.b) * (kk + 1) + en.j;
-                const uint32_t d = reinterpret_cast<const uint32_t*>(&en.a)[lane];
-                const unsigned long long v = (static_cast<unsigned long long>(tag) << 32) | d;
-                asm volatile("st.relaxed.gpu.global.u64 [%0], %1;"
-                             ::"l"(P.partT + (pos * nch + en.c) * 10 + lane), "l"(v) : "memory");
-            }
-            if (nch == 1 && !end) {                              // decide here: nothing to wait for
-                if (lane == 0) s_all[0] = en.a;
-                __syncwarp();
-                const Comb C = combine_parts<GREEDY, true>(s_all, 1, lane);
-                if (!(C.flags & kPartSkipped) && lane == 0) decide<GREEDY>(P, en.b, en.j, en.x, C);
-                __syncwarp();
-            } else if (end || en.c == nch - 1) {                 // queue the row (or the end)
-                const int q = static_cast<int>(nd % kPipeDQ);
-                if (nd >= kPipeDQ) pipe_wait(&dq_empty[q], ((nd / kPipeDQ) & 1u) ^ 1u);
-                if (lane == 0) {
-                    dq[q] = make_int4(en.b, en.j, en.x, end ? 1 : 0);
-                    mbar_arrive(&dq_full[q]);
-                }
-                ++nd;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&pq_empty[e]);
-            if (end) break;
-        }
-        return;
-    }
-
-    if (warp == DW) {
-        // ---------------------------------------------------------------- decider warp
-        // rows in the order their last chunk was published here: poll the row's tagged partials
-        // (each chunk is published by a CTA whose pipeline never waits on a decision, so they
-        // arrive), combine, decide
-        for (uint32_t nd = 0;; ++nd) {
-            const int q = static_cast<int>(nd % kPipeDQ);
-            pipe_wait(&dq_full[q], (nd / kPipeDQ) & 1u);
-            const int4 r = dq[q];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&dq_empty[q]);
-            if (r.w) break;
-            const size_t pos = static_cast<size_t>(r.x) * (kk + 1) + r.y;
-            bool ok = true;
-            for (int cc = lane; cc < nch; cc += 32) {
-                PartA a;
-                ok = spin_until([&] { return read_tagged(P, pos, cc, tag, a); }, 11) && ok;
-                s_all[cc] = a;
-            }
-            ok = __all_sync(0xFFFFFFFFu, ok);
-            __syncwarp();
-            Comb C = combine_parts<GREEDY, true>(s_all, nch, lane);
-            if (!ok) C.flags |= kPartProtocol;
-            if (!(C.flags & kPartSkipped) && lane == 0) decide<GREEDY>(P, r.x, r.y, r.z, C);
-            __syncwarp();
-        }
-        return;
-    }
-
-    // -------------------------------------------------------------------- consumer groups
-    const int g = warp / kWarps, w = warp - g * kWarps, lt = tid - g * kThreads;
-    for (uint32_t n = g;; n += kPipeGroups) {
-        const int sl = static_cast<int>(n % NS);
-        const uint32_t ph = (n / NS) & 1u;
-        pipe_wait(&full[sl][0], ph);
-        const int4 m = meta[sl];                                 // (c, b, j, x)
-        if (m.x < 0) {                                           // end marker
-            if (m.x == -1 && lt == 0) {
-                const int e = static_cast<int>(n % kPipeNQ);
-                if (n >= kPipeNQ) pipe_wait(&pq_empty[e], ((n / kPipeNQ) & 1u) ^ 1u);
-                pq[e].c = -1;
-                mbar_arrive(&pq_full[e]);
-            }
-            return;
-        }
-        pipe_wait(&full[sl][1], ph);
-        const int c = m.x, j = m.z, x = m.w;
-        const int c0 = c * P.CH;
-        const int len = min(P.CH, P.V - c0);
-        const bool load_q = !GREEDY && j < kk && P.qmeta == nullptr;
-        const E* sp = reinterpret_cast<const E*>(smem + static_cast<size_t>(sl) * SLOT);
-        const E* sq = reinterpret_cast<const E*>(smem + static_cast<size_t>(sl) * SLOT + kMaxChunkBytes);
-        const int nfull = len / VEC, nvv = (len + VEC - 1) / VEC;
-        auto unpack = [&](const E* src, float (&v)[NV][VEC]) {
-#pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                const int gv = lt + i * kThreads;
-                if (gv < nfull) {
-                    EL::unpack(*reinterpret_cast<const uint4*>(src + gv * VEC), v[i]);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < VEC; ++e) v[i][e] = -INFINITY;
-                    if (gv < nvv) {
-#pragma unroll
-                        for (int e = 0; e < VEC; ++e)
-                            if (gv * VEC + e < len) v[i][e] = EL::one(src, gv * VEC + e);
-                    }
-                }
-            }
-        };
-        float vp[NV][VEC];
-        unpack(sp, vp);
-        float zxp = 0.0f, zxq = 0.0f;
-        const bool hasx = lt == 0 && x >= c0 && x < c0 + len;
-        if (hasx) zxp = EL::one(sp, x - c0);
-        int nf = 0;
-        float dP = -INFINITY, dQ = -INFINITY, sP = 0.0f, sQ = 0.0f;
-        float gbest = -INFINITY;
-        int gidx = INT_MAX;
-        if (GREEDY) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[sl]);              // the slot is in registers
-            float nanacc = -INFINITY;
-#pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                float vm = -INFINITY;
-#pragma unroll
-                for (int e = 0; e < VEC; e += 2) {
-                    nanacc = max3nan(nanacc, vp[i][e], vp[i][e + 1]);
-                    vm = max3(vm, vp[i][e], vp[i][e + 1]);
-                }
-                if (vm > gbest) {
-                    int fe = 0;
-#pragma unroll
-                    for (int e = VEC - 1; e >= 0; --e)
-                        if (vp[i][e] == vm) fe = e;
-                    gbest = vm;
-                    gidx = c0 + (lt + i * kThreads) * VEC + fe;
-                }
-            }
-            if (!(nanacc < INFINITY)) nf |= kPartNonfiniteP;
-        } else {
-            float vq[NV][VEC];
-            if (load_q) {
-                unpack(sq, vq);
-                if (hasx) zxq = EL::one(sq, x - c0);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[sl]);              // the slot is in registers
-            thread_stats<NV, VEC>(vp, P.c2, kPartNonfiniteP, dP, sP, nf);
-            if (load_q) thread_stats<NV, VEC>(vq, P.c2, kPartNonfiniteQ, dQ, sQ, nf);
-        }
-        // block reduction over the group's 8 warps without a barrier: every warp stores its
-        // partial, the last of the eight (a shared-memory counter) combines.  A warp runs at most
-        // two of its group's entries ahead of the slowest one (a slot is reloaded only after all
-        // eight released it), so RB = 4 scratch sets never collide.
-        const int bf = static_cast<int>((n / kPipeGroups) % RB);
-        nf = __reduce_or_sync(0xFFFFFFFFu, nf);
-        if (GREEDY) {
-            float v = gbest;
-            int ii = gidx;
-            warp_argmax(v, ii);
-            if (lane == 0) {
-                r_d[g][bf][0][w] = v;
-                r_gi[g][bf][w] = ii;
-                r_f[g][bf][w] = nf;
-            }
-        } else {
-            const float Dw = warp_max(dP), Ew = warp_max(dQ);
-            const double Sw = warp_sum(sP > 0.0f ? static_cast<double>(sP * ex2_approx(dP - Dw)) : 0.0);
-            const double Tw = warp_sum(sQ > 0.0f ? static_cast<double>(sQ * ex2_approx(dQ - Ew)) : 0.0);
-            if (lane == 0) {
-                r_d[g][bf][0][w] = Dw;
-                r_d[g][bf][1][w] = Ew;
-                r_s[g][bf][0][w] = Sw;
-                r_s[g][bf][1][w] = Tw;
-                r_f[g][bf][w] = nf;
-            }
-        }
-        if (lt == 0) {   // the chunk holds x: its logits (read before the slot was released)
-            r_zx[g][bf][0] = hasx ? zxp : 0.0f;
-            r_zx[g][bf][1] = hasx && load_q ? zxq : 0.0f;
-            r_f[g][bf][w] |= hasx ? kPartHasX : 0;
-        }
-        uint32_t old = 0;
-        if (lane == 0) {
-            __threadfence_block();
-            old = atomicAdd(&r_cnt[g][bf], 1u);
-            __threadfence_block();
-        }
-        old = __shfl_sync(0xFFFFFFFFu, old, 0);
-        if (old % kWarps != kWarps - 1) continue;                // not the last warp of the entry
-        PartA pa{};
-        const bool on = lane < kWarps;
-        const int f = __reduce_or_sync(0xFFFFFFFFu, on ? ld_volatile_i32(&r_f[g][bf][lane]) : 0);
-        if (GREEDY) {
-            float v = on ? ld_volatile_f32(&r_d[g][bf][0][lane]) : -INFINITY;
-            int ii = on ? ld_volatile_i32(&r_gi[g][bf][lane]) : INT_MAX;
-            warp_argmax(v, ii);
-            pa.M_p = v;
-            pa.M_q = -INFINITY;
-            pa.S_p = pa.S_q = 0.0;
-            pa.argmax = ii;
-        } else {
-            const float wd = on ? ld_volatile_f32(&r_d[g][bf][0][lane]) : -INFINITY;
-            const float we = on ? ld_volatile_f32(&r_d[g][bf][1][lane]) : -INFINITY;
-            const double ws = on ? ld_volatile_f64(&r_s[g][bf][0][lane]) : 0.0;
-            const double wt = on ? ld_volatile_f64(&r_s[g][bf][1][lane]) : 0.0;
-            const float Dc = warp_max(wd), Ec = warp_max(we);
-            pa.S_p = warp_sum(ws > 0.0 ? ws * static_cast<double>(ex2_approx(wd - Dc)) : 0.0);
-            pa.S_q = warp_sum(wt > 0.0 ? wt * static_cast<double>(ex2_approx(we - Ec)) : 0.0);
-            pa.M_p = Dc;
-            pa.M_q = Ec;
-            pa.argmax = INT_MAX;
-        }
-        if (lane == 0) {
-            pa.zx_p = ld_volatile_f32(&r_zx[g][bf][0]);
-            pa.zx_q = ld_volatile_f32(&r_zx[g][bf][1]);
-            pa.flags = f;
-            const int e = static_cast<int>(n % kPipeNQ);
-            if (n >= kPipeNQ) pipe_wait(&pq_empty[e], ((n / kPipeNQ) & 1u) ^ 1u);
-            pq[e].a = pa;
-            pq[e].c = m.x;
-            pq[e].b = m.y;
-            pq[e].j = m.z;
-            pq[e].x = x;
-            mbar_arrive(&pq_full[e]);
-        }
-    }
-}
-
-// ------------------------------------------------------------------------------------------
 // Kernel B (one CTA per request): residual (or bonus) inverse-CDF sample at the stop position L.
 //
 // The CTA streams row L of its request -- units of kSUnit logits of p_L and q_L -- through a ring
@@ -1983,13 +1430,6 @@ __global__ void __launch_bounds__(kSThreadsB + 32, 1) k_sample_req(const Params 
         primary_done();
         if (tid == 0) s_state = __ldcg(P.state + b);
         __syncthreads();
-    }
-    if (P.fsample && (__ldcg(P.claimed + b) >> 63)) {   // sampled by k_row_stats' chunk tasks
-        if (tid == 0) {
-            atomicAdd(P.epoch + 1, 1u);   // workspace word 1: requests sampled by fused tasks
-            reset_request(P, b);
-        }
-        return;
     }
     const bool lost = s_state == ~0ull;                  // (a wait timed out: protocol fault)
     const uint32_t mask = static_cast<uint32_t>(s_state >> 32);
@@ -2393,43 +1833,8 @@ static void launch_stats_cl(const Params& P, cudaStream_t st) {
     cfg.numAttrs = na;
     cudaLaunchKernelEx(&cfg, k_row_stats<E, G, CL, TAG>, P);
 }
-template <typename E, bool G, int NG>
-static cudaError_t launch_stats_pipe(const Params& P, cudaStream_t st) {
-    static std::atomic<uint64_t> optin{0};
-    static std::atomic<int> sms_cache[64];
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    e = ensure_smem_optin(k_row_pipe<E, G, NG>, pipe_ring<NG>(), optin);
-    if (e != cudaSuccess) return e;
-    int sms = sms_cache[dev & 63].load(std::memory_order_relaxed);
-    if (sms == 0) {
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        sms_cache[dev & 63].store(sms, std::memory_order_relaxed);
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(sms * pipe_cps<NG>()));
-    cfg.blockDim = dim3(pipe_threads<NG>());
-    cfg.dynamicSmemBytes = pipe_ring<NG>();
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    int na = 0;
-    if (P.chain) {
-        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
-    cfg.attrs = attr;
-    cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, k_row_pipe<E, G, NG>, P);
-}
 template <typename E, bool G>
 static void launch_stats(const Params& P, cudaStream_t st) {
-    if (P.pipe) {                  // (pipelined persistent CTAs)
-        if (P.pipe == 2) launch_stats_pipe<E, G, 2>(P, st);
-        else launch_stats_pipe<E, G, 3>(P, st);
-        return;
-    }
     if (P.tagpub) {   // (tagged partials: rows of 2..64 chunks without clusters)
         launch_stats_cl<E, G, 1, true>(P, st);
         return;

@@ -236,16 +236,13 @@ def test_gpu_monte_carlo_matches_exact_outcome():
     ({"STARSD_ROWCLUSTER": "-8"}, ("two_launch", 8)),       # clusters of 8 on every row (G > 1)
     ({"STARSD_ROWCLUSTER": "-2"}, ("two_launch", 2)),
     ({"STARSD_PUBLISH_TICKET": "1"}, ("two_launch", 0)),   # release-ordered partials + row ticket
-    ({"STARSD_FUSED_SAMPLE": "0"}, ("two_launch", 0)),     # every request sampled by the tail
     ({"STARSD_RGROUP": "5"}, ("two_launch", 0)),           # group-major k_row_stats grid
-    ({"STARSD_PIPE": "1"}, ("two_launch", 0)),             # pipelined persistent k_row_pipe
-    ({"STARSD_PIPE": "1", "STARSD_EARLY": "0"}, ("two_launch", 0)),
     ({"STARSD_EARLY": "0"}, ("two_launch", 0)),            # sampler after k_row_stats completes
 ])
 def test_kernel_variants_match_the_oracle(env, want):
     """Kernel variants chosen by environment (once per process, so in a subprocess) against the
-    oracle on the default path's cases plus a Llama-3-vocabulary case: every sampling chunk task
-    in the tail kernel (no fused tasks), the cluster-free k_row_stats (tagged partials), forced
+    oracle on the default path's cases plus a Llama-3-vocabulary case: the tail sampler after
+    k_row_stats completes (no early launch), the cluster-free k_row_stats (tagged partials), forced
     clusters whose row partials meet through the global ticket (G = ceil(nch / CL) > 1), and the
     ticket publish."""
     import json

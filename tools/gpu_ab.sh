@@ -12,9 +12,6 @@ for cfg in $CFGS; do
   for v in $VARIANTS; do
     case $v in
       base) E="";;
-      FUSED0) E="STARSD_FUSED_SAMPLE=0";;
-      PIPE) E="STARSD_PIPE=1";;
-      PIPE2) E="STARSD_PIPE=2";;
       EARLY0) E="STARSD_EARLY=0";;
       TICKET) E="STARSD_PUBLISH_TICKET=1";;
       RG*) E="STARSD_RGROUP=${v#RG}";;
@@ -25,7 +22,7 @@ for cfg in $CFGS; do
 import json
 try:
     d=json.loads(open("gpurun_out/ab_${cfg}_$v.json").read().strip().splitlines()[-1]); r=d["roofline"]
-    print("$cfg $v", "step %.1f us" % (d["ms_per_step"]*1e3), "kA %.1f ev %.1f" % (r["kernel_ms_mean"]*1e3, r["kernel_ms_events"]*1e3), "frac %.3f step_frac %.3f" % (r["frac"], r["step_frac"]), "fused %.3f" % d["accept"].get("fused_sampled_frac", -1), "clk", d["clocks"]["sm_mhz"])
+    print("$cfg $v", "step %.1f us" % (d["ms_per_step"]*1e3), "kA %.1f ev %.1f" % (r["kernel_ms_mean"]*1e3, r["kernel_ms_events"]*1e3), "frac %.3f step_frac %.3f" % (r["frac"], r["step_frac"]), "clk", d["clocks"]["sm_mhz"])
 except Exception as e:
     print("$cfg $v FAILED", e, open("gpurun_out/ab_${cfg}_$v.err").read()[-800:])
 PY
