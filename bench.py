@@ -188,6 +188,37 @@ def oracle_rate(d, T, seconds, seed, cores, per_step=None, steps=None):
     return tok / el, dict(requests=n, steps=i, per_step=per_step, seconds=el)
 
 
+def parity_sample(dev_batch, d0, T, V, cores, n=32):
+    """After the timed region: one GPU verify of batch 0 (seed 21622, round 0) against the oracle
+    on its first n requests, with the C-13 rule (tests/parity.py): exact unless the oracle's fp64
+    margins are below 1e-6 (a tie).  Returns the counts (mismatches must be 0)."""
+    import numpy as np
+    import torch
+    import oracle
+    import paper_2601_21622_b200 as sd
+    L, tok, st = sd.verify(dev_batch["p"], None if T == 0 else dev_batch["q"], dev_batch["ids"], T,
+                           seed=21622, round=0, request_id_base=0, vocab=V)
+    torch.cuda.synchronize()
+    n = min(n, int(L.shape[0]))
+    gL, gt, gs = L[:n].cpu().numpy(), tok[:n].cpu().numpy(), st[:n].cpu().numpy()
+    rL, rt, rs, tr = oracle.verify(d0["p"][:n], None if T == 0 else d0["q"][:n], d0["ids"][:n], T,
+                                   seed=21622, round=0, rid_base=0, V=V, trace=True,
+                                   n_threads=cores)
+    exact = ties = bad = 0
+    for b in range(n):
+        same = gL[b] == rL[b] and np.array_equal(gt[b], rt[b]) and gs[b] == rs[b]
+        tie = T > 0 and not (rs[b] & oracle.HARD_FAULTS) and (
+            tr[b].mu_a < 1e-6 or tr[b].mu_s < 1e-6 or tr[b].R < 5e-8)
+        if same:
+            exact += 1
+        elif tie:
+            ties += 1
+        else:
+            bad += 1
+    return {"requests": n, "bit_exact": exact, "ties": ties, "mismatches": bad,
+            "rule": "C-13 (DESIGN.md): bit-exact L, tokens, status outside fp64 margins < 1e-6"}
+
+
 def host_batch(d):
     import numpy as np
     import torch
@@ -435,7 +466,8 @@ def run_ours(args):
                "sample": f"{info['requests']} requests of batch 0 ({info['steps']} calls x "
                          f"{info['per_step']}), {info['seconds']:.1f} s on {cores} threads",
                "single_core": {"value": rate1, "cores": 1,
-                               "sample": f"{info1['requests']} requests, {info1['seconds']:.1f} s"}}
+                               "sample": f"{info1['requests']} requests, {info1['seconds']:.1f} s"},
+               "parity_sample": parity_sample(batches[0], d0, T, V, cores)}
 
     if rank == 0:
         clocks = clk.summary()
@@ -458,6 +490,7 @@ def run_ours(args):
             "kernel_plan": pl,
             "clocks": clocks,
             "accept": {"mean_L": float(Lh.mean()), "mean_emitted": float((Lh + 1).mean()),
+                       "L_hist": np.bincount(Lh.ravel().astype(np.int64), minlength=k + 1).tolist(),
                        "fault_requests": int((~ok).sum())},
         }
         print(json.dumps(line), flush=True)
