@@ -95,3 +95,19 @@ def test_tree_walk_distribution_matches_the_exact_outcome():
     keep = exact * R > 5
     g = 2 * np.sum(obs[keep] * np.log(np.maximum(obs[keep], 1) / (R * exact[keep])))
     assert stats.chi2.sf(g, keep.sum() - 1) > 1e-4
+
+
+def test_tree_verify_one_cta_kernel_matches_the_oracle():
+    """STARSD_TREE_CLUSTER=0 -- the one-CTA-per-request tree kernel instead of the 8-CTA cluster
+    (the knob is read once per process, so in a subprocess): the same parity cases as above."""
+    if os.environ.get("STARSD_TREE_CLUSTER") == "0":
+        pytest.skip("(running inside the subprocess)")
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
+                        os.path.abspath(__file__), "-k", "matches_the_oracle and not one_cta"],
+                       env=dict(os.environ, STARSD_TREE_CLUSTER="0"), capture_output=True, text=True,
+                       timeout=900, cwd=root)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "6 passed" in r.stdout, r.stdout[-1000:]
